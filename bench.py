@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""Benchmark: EC / surface-area / volume curves of a 3D float32 Gaussian
+random field (BASELINE.json configs[4]: 2048^3, sigma = 4 voxels, 512 levels,
+z-slab partitioned over N GPUs with one NCCL all-reduce of the histograms).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1)
+
+One step = one pass of the hot path over the whole field: fused quantize +
+2x2x2 transition-class histogram kernel on this rank's z-slab (+1 halo
+plane), NCCL all-reduce of the histogram (N > 1), device finalize into the
+three curves.  ``value`` is whole-job Gvoxels/s with the field resident in HBM
+(max over ranks of the CUDA-event time); ``e2e`` is the same through the public
+API (``descriptor_curves`` on an ``ArraySource`` over PINNED HOST memory:
+chunked H2D overlapped with the kernel, curves read back to the host).
+``--impl reference`` times the reference algorithm on the host CPU cores (the
+C restatement in oracle/, all threads) on a bounded sample of the same field.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: (shape, sigma, M, dtype, descriptors)
+    "c5": ((2048, 2048, 2048), 4.0, 511, "f32", ("ec", "surface-area", "volume")),
+    "c4a": ((512, 512, 512), 3.0, 255, "f32", ("ec", "surface-area", "volume")),
+    "small": ((256, 256, 256), 3.0, 255, "f32", ("ec", "surface-area", "volume")),
+}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v.strip().lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_reference(x_host, M, lo_hi, descs, budget_s=15.0, threads=None):
+    """Oracle (C restatement of the reference gather, all host threads) on a
+    bounded slab sample of the field; returns (Gvoxels/s, cells, seconds, threads)."""
+    from oracle import oracle
+    threads = threads or os.cpu_count() or 1
+    H, W, D = x_host.shape
+    tables = [oracle.BUILTIN_3D[(d, "26C" if d == "ec" else None)] for d in descs]
+
+    def run(nplanes):
+        sample = np.ascontiguousarray(x_host[:nplanes])
+        t0 = time.perf_counter()
+        q_in, q_out = oracle.gather3d(sample, M, value_range=lo_hi, workers=threads, rows=(0, nplanes))
+        for w in tables:
+            oracle.descriptor_numerators(q_in, q_out, M, w)
+        return time.perf_counter() - t0
+
+    n = 2
+    t = run(n)
+    while t < 0.5 and n < H:
+        n = min(H, n * 4)
+        t = run(n)
+    n_final = max(1, min(H, int(n * budget_s / max(t, 1e-6))))
+    t = run(n_final)
+    cells = n_final * W * D
+    return cells / t / 1e9, cells, t, threads
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c5")
+    ap.add_argument("--seed", type=int, default=2311)
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: W >= 3 is the contract; raising warmup to 3", file=sys.stderr)
+        args.warmup = 3
+
+    import torch
+    ws, rank, local = dist_env()
+    shape, sigma, M, _, descs = CONFIGS[args.config]
+    H, W, D = shape
+    config = {"workload": f"{args.config}: 3D float32 smoothed Gaussian random field {H}x{W}x{D}, "
+                          f"sigma={sigma:g} voxels, min-max normalised, {M + 1} levels; "
+                          f"curves: {', '.join(descs)}",
+              "field": [H, W, D], "sigma": sigma, "levels": M + 1, "descriptors": list(descs),
+              "partition": f"z-slabs over {ws} rank(s), 1-plane halo" + (", NCCL all-reduce" if ws > 1 else ""),
+              "l2": "inputs larger than L2 (field >> 126 MB)"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        run_reference(args, shape, sigma, M, descs, config, ws)
+        return
+
+    import paper_2311_11740_b200 as ft
+    from paper_2311_11740_b200 import engine, synth
+    from paper_2311_11740_b200._parallel import split_blocks
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    blocks = split_blocks(H + 1, ws)
+    a, b = blocks[rank] if rank < len(blocks) else (H + 1, H + 1)
+    r0, r1 = max(a - 1, 0), min(b - 1, H - 1) + 1
+
+    # ---- field (setup, untimed) -------------------------------------------
+    x = synth.grf_slab(shape, sigma, args.seed, (r0, r1), dev)
+    mn, mx = x.min(), x.max()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.all_reduce(mn, op=dist.ReduceOp.MIN)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    synth.normalise_(x, mn, mx)
+    torch.cuda.synchronize()
+
+    quant = ft.quant.QuantSpec.for_range(0.0, 1.0, M)
+    tables = [ft.builtin_weights(d, "26C") for d in descs]
+    eighths = [t.eighths for t in tables]
+    hist = engine.new_hist(3, M, dev)
+    stream = torch.cuda.current_stream(dev)
+    k_start, k_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kernel_ms = []
+
+    def step(timed_kernel=False):
+        hist.zero_()
+        if timed_kernel:
+            k_start.record(stream)
+        engine.launch_hist(3, x, shape, M, quant, rows=(a, b), first=r0, hist=hist)
+        if timed_kernel:
+            k_end.record(stream)
+        if ws > 1:
+            import torch.distributed as dist
+            dist.all_reduce(hist)
+        _, _, num = engine.finalize(3, M, hist, maps=False, tables=eighths)
+        return num
+
+    def barrier():
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for _ in range(args.steps):
+            step()
+        t1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = t0.elapsed_time(t1) / args.steps
+    # kernel-only durations (dominant kernel, for the roofline), separate pass
+    for _ in range(max(3, args.steps // 2)):
+        step(timed_kernel=True)
+        torch.cuda.synchronize()
+        kernel_ms.append(k_start.elapsed_time(k_end))
+    kms = statistics.median(kernel_ms)
+    t_ms = torch.tensor([ms, kms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+    ms, kms = t_ms.tolist()
+    cells = H * W * D
+    value = cells / (ms / 1e3) / 1e9
+
+    # ---- end to end through the public API, host-resident input ----------
+    e2e = None
+    if not args.no_e2e:
+        e2e_steps = args.e2e_steps or max(1, min(args.steps, 3))
+        host = torch.empty(x.shape, dtype=torch.float32, pin_memory=True)
+        host.copy_(x)
+        del x
+        torch.cuda.empty_cache()
+        src = ft.ArraySource(host.numpy(), M, value_range=(0.0, 1.0))
+        # the rank's planes [r0, r1) stand for global planes; shift the vertex rows
+        local_src = _ShiftedSource(src, r0, H)
+        e_times = []
+        for it in range(1 + e2e_steps):
+            barrier()
+            torch.cuda.synchronize()
+            s = time.perf_counter()
+            h = ft.gather.stream_hist(local_src, 3, dev, (a, b), chunk_bytes=512 << 20)
+            if ws > 1:
+                import torch.distributed as dist
+                dist.all_reduce(h)
+            _, _, num = engine.finalize(3, M, h, maps=False, tables=eighths)
+            curves = num.cpu().numpy()
+            torch.cuda.synchronize()
+            if it:
+                e_times.append(time.perf_counter() - s)
+        et = torch.tensor([statistics.mean(e_times)], dtype=torch.float64, device=dev)
+        if ws > 1:
+            import torch.distributed as dist
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(cells / et.item() / 1e9, 4), "unit": "Gvoxels/s",
+               "h2d_bytes_per_step": int((r1 - r0) * W * D * 4 * ws), "d2h_bytes_per_step": int(curves.nbytes),
+               "path": "descriptor_curves-equivalent: ArraySource over pinned host memory, 512 MiB chunks, "
+                       "double-buffered H2D overlapped with the kernel, curves to host"}
+        x = None
+
+    # ---- CPU baseline (rank 0, N = 1 only) ----------------------------------
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        xs = host.numpy() if e2e is not None else x.cpu().numpy()
+        v, n, secs, thr = cpu_reference(xs, M, (0.0, 1.0), descs, args.cpu_budget)
+        cpu = {"value": round(v, 6), "unit": "Gvoxels/s", "cores": thr, "kind": "port",
+               "sample": f"{n // (W * D)} planes x {W}x{D} of the same field ({n} voxels, {secs:.1f} s), "
+                         "oracle/ft_oracle.c gather + curves"}
+
+    if rank == 0:
+        peak, peak_kind = peaks()
+        # algorithmic bytes: every cell of the rank's planes read once (f32)
+        bytes_per_launch = (r1 - r0) * W * D * 4
+        achieved = bytes_per_launch / (kms / 1e3) / 1e9
+        out = {"metric": "Gvoxels/s for EC curve (1/2/4/8 B200) and % of HBM roofline vs CPU ref",
+               "value": round(value, 4), "unit": "Gvoxels/s", "n_gpus": ws, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+               "scaling": "strong", "vs_baseline": None, "dtype": "f32 in, int32 levels, u64 histograms",
+               "data": "synthetic (seeded device-generated GRF; no dataset in the reference)",
+               "config": config,
+               "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+                            "frac": round(achieved / peak, 4), "traffic": None,
+                            "kernel": "hist3d_tiled (+edge), per-launch median over CUDA events",
+                            "kernel_ms": round(kms, 4), "peak_source": peak_kind,
+                            "algorithmic_bytes_per_launch": int(bytes_per_launch)},
+               "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": 3 * args.steps,
+               "clocks": clk.summary()}
+        print(json.dumps(out))
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+class _ShiftedSource:
+    """Present a host array holding global planes [r0, r0 + n) as the full
+    field (reads only ever touch the rank's planes)."""
+
+    mode = "file-backed"
+
+    def __init__(self, src, r0, H):
+        self.src, self.r0, self.H = src, r0, H
+        self.ndim, self.max_level, self.quant, self.dtype = 3, src.max_level, src.quant, src.dtype
+        self.height, self.width, self.depth = H, src.width, src.depth
+        self.shape = (H, src.width, src.depth)
+        self.peak_field_bytes = 0
+
+    def note_resident(self, n):
+        self.peak_field_bytes = max(self.peak_field_bytes, n)
+
+    def read_rows(self, a, b, out):
+        self.src.read_rows(a - self.r0, b - self.r0, out)
+
+
+def run_reference(args, shape, sigma, M, descs, config, ws):
+    """CPU baseline arm: the reference algorithm (oracle/ft_oracle.c, a C
+    restatement of fieldtopo's Numba kernels) on all host cores."""
+    import torch
+    from paper_2311_11740_b200 import synth
+    H, W, D = shape
+    # same field bytes as our arm: generate on the GPU if present, else a CPU
+    # stand-in of the same distribution; only a bounded slab is needed
+    nplanes = min(H, 64)
+    if torch.cuda.is_available():
+        x = synth.grf_slab(shape, sigma, args.seed, (0, nplanes), torch.device("cuda", 0))
+        x = ((x - x.min()) / (x.max() - x.min())).cpu().numpy()
+    else:
+        x = np.random.default_rng(args.seed).random((nplanes, W, D), dtype=np.float32)
+    times = []
+    for it in range(args.warmup + args.steps):
+        v, n, secs, thr = cpu_reference(x, M, (0.0, 1.0), descs, budget_s=max(2.0, args.cpu_budget / 3))
+        if it >= args.warmup:
+            times.append(v)
+    v = statistics.mean(times)
+    out = {"impl": "reference", "metric": "Gvoxels/s for EC curve (1/2/4/8 B200) and % of HBM roofline vs CPU ref",
+           "value": round(v, 6), "unit": "Gvoxels/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32 in, int64 levels",
+           "data": "synthetic (same seeded GRF slab)", "config": config,
+           "cpu_baseline": {"value": round(v, 6), "unit": "Gvoxels/s", "cores": thr, "kind": "port",
+                            "sample": f"{n // (W * D)} planes x {W}x{D} per step (bounded sample)"},
+           "e2e": {"value": round(v, 6), "unit": "Gvoxels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,145 @@
+/*
+ * fieldtopo_b200.h -- C ABI of the B200-native vertex-contribution engine.
+ *
+ * Drop-in boundary for the hot path of the reference package `fieldtopo`
+ * (arXiv 2311.11740).  The reference's native layer is three Numba kernels
+ * that accumulate birth/death histograms in place; each entry point below
+ * replaces one of them (or the numpy pass after them) with a stream-ordered
+ * CUDA launch on device memory.  Plain pointers and sizes only: no torch or
+ * CUDA C++ types cross this boundary (`stream` is a cudaStream_t passed as
+ * void*; NULL = legacy default stream).
+ *
+ * Conventions:
+ *   return 0 = ok, 1 = bad argument (-> ValueError), 2 = classification
+ *   failure (-> ClassificationError), >= 1000 = CUDA error 1000 + cudaError_t
+ *   (-> RuntimeError).  The library never frees caller memory; histogram
+ *   outputs are ACCUMULATED (+=) exactly like the reference kernels' q_in/q_out
+ *   arguments, so callers zero them first.  Calls are asynchronous on
+ *   `stream`; all arguments are read before the call returns.
+ */
+#ifndef FIELDTOPO_B200_H
+#define FIELDTOPO_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FT_OK 0
+#define FT_ERR_ARG 1
+#define FT_ERR_CLASSIFY 2
+#define FT_ERR_CUDA_BASE 1000
+
+/* element type of a field buffer */
+#define FT_I32 0 /* int32 levels (Field2D/Field3D values, fields.py:17) */
+#define FT_U8 1
+#define FT_U16 2
+#define FT_F32 3
+#define FT_F64 4 /* ft_quantize / ft_minmax only (thresholds are then doubles) */
+
+/* level decoding */
+#define FT_Q_IDENTITY 0     /* the element IS the level */
+#define FT_Q_TABLE 1        /* quantize_with_range via threshold table (fast) */
+#define FT_Q_TABLE_ROBUST 2 /* same, for ill-conditioned ranges */
+
+#define FT_NCLASS_2D 6  /* transition classes, 2D */
+#define FT_NCLASS_3D 40 /* transition classes, 3D */
+#define FT_NTYPE_2D 5   /* q1 q2 qd q3 q4            (contrib2d.py:36)    */
+#define FT_NTYPE_3D 21  /* q10 .. q80                (contrib3d.py:35-44) */
+
+/* Level decoding of a raw buffer.  For FT_Q_TABLE*: level(x) is the
+ * reference quantize_with_range(x, lo, hi, M) (fields.py:20-33), decided by
+ * `thresholds` (device, M+2 floats: [-inf, t_1 .. t_M, NaN], t_l = smallest
+ * float32 whose reference level is >= l) after the estimate
+ * floor(fmaf(x', scale, bias)), x' = negate ? -x : x. */
+typedef struct ft_quant {
+    int32_t mode;
+    int32_t negate;
+    float scale;
+    float bias;
+    const float *thresholds;
+} ft_quant;
+
+/* A device-resident run of consecutive rows (2D) or planes (3D) of a field
+ * whose full extent is H rows/planes.  Rows/planes outside [0, H) are absent
+ * cells (sentinel M+1, like the reference's padded border, sources.py:66-74);
+ * rows/planes inside [0, H) that a launch needs must lie in
+ * [first, first + count).  Element (r, ...) lives at
+ * data + ((r - first) * row_elems + ...) + b * batch_stride. */
+typedef struct ft_window {
+    const void *data;
+    int32_t dtype;
+    int64_t first;
+    int64_t count;
+    int64_t batch;        /* 2D only: images sharing H x W; else 1 */
+    int64_t batch_stride; /* elements between consecutive images */
+} ft_window;
+
+/* 2D transition histograms for vertex rows [v0, v1) (0 <= v0 <= v1 <= H+1)
+ * of an H x W field (row-major, W contiguous).  hist: device uint64
+ * [batch][6][M+2], accumulated.  Replaces _scan_rows_2d(padded, i0, i1, q_in,
+ * q_out) (contrib2d.py:161-162) and its two-row streaming window
+ * (_stream_rows_2d, contrib2d.py:235-251). */
+int ft_hist2d(const ft_window *win, int64_t H, int64_t W, int64_t v0, int64_t v1,
+              const ft_quant *q, int32_t M, uint64_t *hist, void *stream);
+
+/* 3D transition histograms for vertex rows [v0, v1) of an H x W x D field
+ * (index (i, j, k), k fastest; raw layout (i*W + j)*D + k, sources.py:379-386).
+ * hist: device uint64 [40][M+2], accumulated.  Replaces _scan_slabs_3d
+ * (contrib3d.py:351-352) and _scan_pencil_pair_3d / _stream_slabs_3d
+ * (contrib3d.py:373-414). */
+int ft_hist3d(const ft_window *win, int64_t H, int64_t W, int64_t D, int64_t v0, int64_t v1,
+              const ft_quant *q, int32_t M, uint64_t *hist, void *stream);
+
+/* Transition histograms -> contribution maps and descriptor curves.
+ * hist [batch][C][M+2] (C = 6 or 40).  q_in / q_out (may be NULL): device
+ * uint64 [batch][T][M+2], OVERWRITTEN with the reference maps
+ * (ContributionMap2D/3D.q_in/q_out, contrib2d.py:45-105, contrib3d.py:138-200).
+ * class_w: device int64 [n_desc][C] per-class curve deltas in eighths
+ * (w[dst] - w[src], see ft_class_weights); numerators: device int64
+ * [batch][n_desc][M+1] OVERWRITTEN with descriptor_curve(...).numerators
+ * (counts_at_levels + eighths @ counts, descriptors.py:153-178) computed as a
+ * device prefix scan over levels. */
+int ft_finalize(int32_t ndim, int32_t M, int64_t batch, const uint64_t *hist, uint64_t *q_in,
+                uint64_t *q_out, int32_t n_desc, const int64_t *class_w, int64_t *numerators,
+                void *stream);
+
+/* Generic weighted level prefix scan: numerators[b][d][l] =
+ * sum_{l' <= l} sum_r row_w[d][r] * rows[b][r][l'] for l in [0, M]; rows:
+ * device uint64 [batch][n_rows][M+2], row_w: device int64 [n_desc][n_rows].
+ * With rows = (q_in; q_out) and row_w = (eighths; -eighths) this is
+ * descriptor_curve(cmap, table).numerators (descriptors.py:169-178); with
+ * one-hot weights it is counts_at_levels (descriptors.py:153-161). */
+int ft_curves(const uint64_t *rows, int32_t n_rows, int32_t M, int64_t batch, int32_t n_desc,
+              const int64_t *row_w, int64_t *numerators, void *stream);
+
+/* Per-class curve deltas for a weight table in eighths (WeightTable.eighths,
+ * descriptors.py:27-48): out[c] = eighths[dst(c)] - eighths[src(c)] (host). */
+int ft_class_weights(int32_t ndim, const int64_t *eighths, int64_t *out);
+
+/* The transition tables compiled into the library (host memory):
+ * step[(1 << S) * S] (class booked when slot joins mask, -1 invalid),
+ * src[C], dst[C] (type index; -1 = empty stage).  S = 4 (2D) or 8 (3D). */
+int ft_tables(int32_t ndim, int32_t *step, int32_t *src, int32_t *dst);
+
+/* quantize_with_range (fields.py:20-33) on device: out[i] = level(x[i]). */
+int ft_quantize(const void *x, int32_t dtype, int64_t n, const ft_quant *q, int32_t M,
+                int32_t *out, void *stream);
+
+/* Device min / max of a buffer (quantize's data range, fields.py:44-45;
+ * RawVolumeSource._scan_range, sources.py:335-347).  out: device uint32[2],
+ * OVERWRITTEN with order-preserving keys of (min, max); decode with
+ * ft_key_to_double (FT_F64: see below). */
+int ft_minmax(const void *x, int32_t dtype, int64_t n, uint32_t *out, void *stream);
+double ft_key_to_double(int32_t dtype, uint32_t key);
+/* FT_F64 buffers: out is uint64[2]; decode with ft_key64_to_double. */
+double ft_key64_to_double(uint64_t key);
+
+/* Library version string. */
+const char *ft_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FIELDTOPO_B200_H */

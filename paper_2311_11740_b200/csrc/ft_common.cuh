@@ -1,0 +1,135 @@
+// ft_common.cuh -- shared device helpers for the fieldtopo-b200 kernels.
+//
+// Level decoding (fused quantize), sorting networks and launch bookkeeping.
+// Everything here is sm_100a device code; see DESIGN.md §3 for the layout.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/fieldtopo_b200.h"
+
+#define FT_CUDA_TRY(expr)                                   \
+    do {                                                    \
+        cudaError_t _e = (expr);                            \
+        if (_e != cudaSuccess) return FT_ERR_CUDA_BASE + (int)_e; \
+    } while (0)
+
+namespace ft {
+
+constexpr int kSMs = 148;
+
+// ------------------------------------------------------------------ loads
+template <int DT> struct Elem;
+template <> struct Elem<FT_I32> { using T = int32_t; };
+template <> struct Elem<FT_U8> { using T = uint8_t; };
+template <> struct Elem<FT_U16> { using T = uint16_t; };
+template <> struct Elem<FT_F32> { using T = float; };
+template <> struct Elem<FT_F64> { using T = double; };
+
+// Streaming read-only load: the field is read once per kernel (halo re-reads
+// hit L2), so keep it out of L1.
+template <typename T>
+__device__ __forceinline__ T ld_stream(const T* p) { return __ldg(p); }
+
+// ------------------------------------------------------------ quantization
+// Quantization state for one launch.  The float64 reference formula
+// (fields.py:20-33) is monotone, so a host-built float32 threshold table
+// tt[0..M+1] (tt[0] = -inf, tt[l] = smallest x with level(x) >= l,
+// tt[M+1] = NaN) decides it exactly: level(x) = #{l >= 1 : x >= tt[l]}.
+// A float32 FMA estimate lands within +-1 of the answer for well-conditioned
+// ranges (host-checked) and one compare on each side fixes it; ill-conditioned
+// ranges use the walking variant.
+struct QuantDev {
+    int mode;        // FT_Q_IDENTITY / FT_Q_TABLE / FT_Q_TABLE_ROBUST
+    int negate;      // reversed range (hi < lo): evaluate on -x
+    float scale, bias;
+    const float* tt; // device, M+2 entries (shared copy made by kernels)
+};
+
+template <int DT, int QM>
+__device__ __forceinline__ uint32_t to_level(typename Elem<DT>::T raw, const float* __restrict__ tt,
+                                             float scale, float bias, int negate, int M)
+{
+    if constexpr (QM == FT_Q_IDENTITY) {
+        // Identity levels are validated on the host (Field2D/Field3D); clamp
+        // to the sentinel so a bad level can never index past the histogram.
+        uint32_t v = (uint32_t)raw;
+        return min(v, (uint32_t)(M + 1));
+    } else {
+        float x = (float)raw;
+        if (negate) x = -x;
+        int est = __float2int_rd(fmaf(x, scale, bias));
+        est = min(max(est, 0), M);
+        if constexpr (QM == FT_Q_TABLE) {
+            est += (x >= tt[est + 1]) ? 1 : 0;
+            est -= (x < tt[est]) ? 1 : 0;
+        } else {
+            while (est < M && x >= tt[est + 1]) ++est;
+            while (est > 0 && x < tt[est]) --est;
+        }
+        return (uint32_t)est;
+    }
+}
+
+// float64 inputs (ft_quantize only): the same scheme with a double table.
+template <int QM>
+__device__ __forceinline__ uint32_t to_level_f64(double x, const double* __restrict__ tt, double scale,
+                                                 double bias, int negate, int M)
+{
+    if (negate) x = -x;
+    double y = fma(x, scale, bias);
+    int est = (y != y) ? 0 : (y <= 0.0 ? 0 : (y >= (double)M ? M : (int)floor(y)));
+    if constexpr (QM == FT_Q_TABLE) {
+        est += (x >= tt[est + 1]) ? 1 : 0;
+        est -= (x < tt[est]) ? 1 : 0;
+    } else {
+        while (est < M && x >= tt[est + 1]) ++est;
+        while (est > 0 && x < tt[est]) --est;
+    }
+    return (uint32_t)est;
+}
+
+// ------------------------------------------------------- sorting networks
+__device__ __forceinline__ void cswap(uint32_t& a, uint32_t& b)
+{
+    uint32_t lo = min(a, b), hi = max(a, b);
+    a = lo;
+    b = hi;
+}
+
+// Optimal 5-comparator network for 4 keys.
+__device__ __forceinline__ void sort4(uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d)
+{
+    cswap(a, b);
+    cswap(c, d);
+    cswap(a, c);
+    cswap(b, d);
+    cswap(b, c);
+}
+
+// Batcher odd-even merge of two sorted 4-sequences (9 comparators).
+__device__ __forceinline__ void merge44(uint32_t* k)
+{
+    // k[0..3] sorted, k[4..7] sorted
+    cswap(k[0], k[4]);
+    cswap(k[1], k[5]);
+    cswap(k[2], k[6]);
+    cswap(k[3], k[7]);
+    cswap(k[2], k[4]);
+    cswap(k[3], k[5]);
+    cswap(k[1], k[2]);
+    cswap(k[3], k[4]);
+    cswap(k[5], k[6]);
+}
+
+// Odd-even merge of two sorted pairs (3 comparators).
+__device__ __forceinline__ void merge22(uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d)
+{
+    cswap(a, c);
+    cswap(b, d);
+    cswap(b, c);
+}
+
+__host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace ft

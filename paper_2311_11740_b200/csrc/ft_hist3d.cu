@@ -1,0 +1,336 @@
+// ft_hist3d.cu -- 3D vertex-contribution transition histograms (map path).
+//
+// Replaces the reference's _scan_slabs_3d / _accum_vertex_3d
+// (contrib3d.py:241-370).  Per vertex (i, j, k) the eight cells
+// (i-1+di, j-1+dj, k-1+dk) are keyed level*8 + slot (slot = di + 2dj + 4dk):
+// sorting the keys reproduces the reference's stable insertion argsort
+// exactly (ties resolve by slot).  Each sorted rank books ONE event into a
+// per-CTA shared-memory histogram keyed by the transition class
+// (type_n -> type_{n+1}, 40 classes) instead of the reference's
+// 15 q_in/q_out increments.
+//
+// Tiling: a CTA owns a TJ x TK tile of vertex columns (j, k)
+// and marches vertex rows i (the slowest, slab axis).  Each step stages one
+// cell plane tile (+1-cell low halo) into shared memory as 16-bit levels,
+// quantizing on the fly; the plane below stays in registers as an
+// already-sorted 4-key list, so each vertex sorts 4 new keys (5 compare-
+// exchanges) and merges (9) instead of sorting 8 (19).  Global loads run two
+// planes ahead of the compute.  Vertex columns j == W or k == D (the
+// high-side boundary) are done by a flat per-vertex kernel.
+#include <algorithm>
+#include <mutex>
+
+#include "ft_common.cuh"
+#include "ft_tables.h"
+
+namespace ft {
+
+constexpr int TJ3 = 8, TK3 = 32, NT3 = TJ3 * TK3;
+constexpr int PW3 = TK3 + 1;          // staged plane tile row pitch
+constexpr int PN3 = (TJ3 + 1) * PW3;  // staged cells per plane (297)
+constexpr int LD3 = (PN3 + NT3 - 1) / NT3;
+constexpr int PF3 = 2;                // planes in flight
+
+struct Geo3 {
+    int64_t H, W, D, v0, v1, first;
+    int M;
+    int tiles_j, tiles_k, chunk;
+    int64_t n_items;
+};
+
+template <int DT, int QM>
+__device__ __forceinline__ uint32_t level3(const typename Elem<DT>::T* __restrict__ buf,
+                                           const Geo3& g, int64_t p, int64_t j, int64_t k,
+                                           const float* tt, const QuantDev& q)
+{
+    if (p < 0 || p >= g.H || j < 0 || j >= g.W || k < 0 || k >= g.D) return (uint32_t)g.M + 1;
+    return to_level<DT, QM>(ld_stream(buf + ((p - g.first) * g.W + j) * g.D + k), tt, q.scale,
+                            q.bias, q.negate, g.M);
+}
+
+__device__ __forceinline__ void book3(uint32_t* __restrict__ h, const uint32_t* __restrict__ trans,
+                                      const uint32_t (&k8)[8], int M2)
+{
+    atomicAdd(&h[k8[0] >> 3], 1u);
+    uint32_t mask = 1u << (k8[0] & 7);
+#pragma unroll
+    for (int r = 1; r < 7; ++r) {
+        const uint32_t s = k8[r] & 7;
+        atomicAdd(&h[trans[(mask << 3) | s] + (k8[r] >> 3)], 1u);
+        mask |= 1u << s;
+    }
+    atomicAdd(&h[39 * M2 + (k8[7] >> 3)], 1u);
+}
+
+__device__ __forceinline__ void init_shared3(uint32_t* h, uint32_t* trans, float* tt, const Step3& step,
+                                             const QuantDev& q, int M2, bool table)
+{
+    for (int i = threadIdx.x; i < 40 * M2; i += blockDim.x) h[i] = 0;
+    for (int i = threadIdx.x; i < 2048; i += blockDim.x) {
+        uint32_t c = step.cls[i];
+        trans[i] = c == 255 ? 0u : c * (uint32_t)M2;
+    }
+    if (table)
+        for (int i = threadIdx.x; i < M2; i += blockDim.x) tt[i] = q.tt[i];
+}
+
+__device__ __forceinline__ void flush_hist(const uint32_t* h, unsigned long long* __restrict__ hist, int n)
+{
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        uint32_t v = h[i];
+        if (v) atomicAdd(&hist[i], (unsigned long long)v);
+    }
+}
+
+template <int DT, int QM>
+__global__ void __launch_bounds__(NT3) hist3d_tiled(const typename Elem<DT>::T* __restrict__ buf,
+                                                    Geo3 g, QuantDev q, Step3 step,
+                                                    unsigned long long* __restrict__ hist)
+{
+    using T = typename Elem<DT>::T;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int M2 = g.M + 2;
+    uint32_t* h = reinterpret_cast<uint32_t*>(smem_raw);
+    uint32_t* trans = h + 40 * M2;
+    float* tt = reinterpret_cast<float*>(trans + 2048);
+    uint16_t* pl = reinterpret_cast<uint16_t*>(tt + M2);
+    init_shared3(h, trans, tt, step, q, M2, QM != FT_Q_IDENTITY);
+    __syncthreads();
+
+    const int tid = threadIdx.x;
+    const int ty = tid / TK3, tx = tid % TK3;
+    const int64_t per_chunk = (int64_t)g.tiles_j * g.tiles_k;
+    const int64_t it0 = g.n_items * blockIdx.x / gridDim.x;
+    const int64_t it1 = g.n_items * (blockIdx.x + 1) / gridDim.x;
+    const uint32_t sentinel = (uint32_t)g.M + 1;
+
+    // staged-cell coordinates of this thread's loads (fixed per tile)
+    int lr[LD3], lc[LD3];
+#pragma unroll
+    for (int e = 0; e < LD3; ++e) {
+        int idx = tid + e * NT3;
+        lr[e] = idx / PW3;
+        lc[e] = idx % PW3;
+    }
+
+    for (int64_t item = it0; item < it1; ++item) {
+        const int64_t ch = item / per_chunk;
+        const int rem = (int)(item - ch * per_chunk);
+        const int64_t j0 = (int64_t)(rem / g.tiles_k) * TJ3;
+        const int64_t k0 = (int64_t)(rem % g.tiles_k) * TK3;
+        const int64_t ia = g.v0 + ch * g.chunk;
+        const int64_t ib = min(ia + (int64_t)g.chunk, g.v1);
+        const bool active = (j0 + ty < g.W) && (k0 + tx < g.D);
+
+        // Raw-value prefetch ring: lv[s] holds the RAW elements of a plane
+        // PF3 - s + 1 steps ahead; levels are produced only when a plane is
+        // stored to shared memory, so the loads stay in flight across steps.
+        T lv[PF3 + 1][LD3];
+        auto inside = [&](int64_t p, int e) {
+            const int64_t jj = j0 - 1 + lr[e], kk = k0 - 1 + lc[e];
+            return (tid + e * NT3 < PN3) && p >= 0 && p < g.H && jj >= 0 && jj < g.W && kk >= 0 && kk < g.D;
+        };
+        auto fetch = [&](int64_t p, T (&dst)[LD3]) {
+#pragma unroll
+            for (int e = 0; e < LD3; ++e) {
+                dst[e] = T(0);
+                if (inside(p, e))
+                    dst[e] = ld_stream(buf + ((p - g.first) * g.W + (j0 - 1 + lr[e])) * g.D + (k0 - 1 + lc[e]));
+            }
+        };
+        auto store = [&](int64_t p, uint16_t* dstp, const T (&src)[LD3]) {
+#pragma unroll
+            for (int e = 0; e < LD3; ++e) {
+                const int idx = tid + e * NT3;
+                if (idx < PN3)
+                    dstp[idx] = (uint16_t)(inside(p, e) ? to_level<DT, QM>(src[e], tt, q.scale, q.bias, q.negate, g.M)
+                                                        : sentinel);
+            }
+        };
+        fetch(ia - 1, lv[0]);
+#pragma unroll
+        for (int s = 1; s <= PF3; ++s) fetch(ia - 1 + s, lv[s]);
+        store(ia - 1, pl, lv[0]);
+        __syncthreads();
+
+        uint32_t lo0 = (uint32_t)pl[ty * PW3 + tx] * 8 + 0;
+        uint32_t lo1 = (uint32_t)pl[(ty + 1) * PW3 + tx] * 8 + 2;
+        uint32_t lo2 = (uint32_t)pl[ty * PW3 + tx + 1] * 8 + 4;
+        uint32_t lo3 = (uint32_t)pl[(ty + 1) * PW3 + tx + 1] * 8 + 6;
+        sort4(lo0, lo1, lo2, lo3);
+
+        for (int64_t i = ia; i < ib; ++i) {
+            uint16_t* cur = pl + ((i - ia + 1) & 1) * PN3;
+            store(i, cur, lv[1]);
+#pragma unroll
+            for (int s = 1; s < PF3; ++s)
+#pragma unroll
+                for (int e = 0; e < LD3; ++e) lv[s][e] = lv[s + 1][e];
+            if (i + PF3 < ib) fetch(i + PF3, lv[PF3]);
+            __syncthreads();
+            uint32_t u0 = (uint32_t)cur[ty * PW3 + tx] * 8 + 1;
+            uint32_t u1 = (uint32_t)cur[(ty + 1) * PW3 + tx] * 8 + 3;
+            uint32_t u2 = (uint32_t)cur[ty * PW3 + tx + 1] * 8 + 5;
+            uint32_t u3 = (uint32_t)cur[(ty + 1) * PW3 + tx + 1] * 8 + 7;
+            sort4(u0, u1, u2, u3);
+            if (active) {
+                uint32_t k8[8] = {lo0, lo1, lo2, lo3, u0, u1, u2, u3};
+                merge44(k8);
+                book3(h, trans, k8, M2);
+            }
+            lo0 = u0 - 1;
+            lo1 = u1 - 1;
+            lo2 = u2 - 1;
+            lo3 = u3 - 1;
+        }
+        __syncthreads();
+    }
+    __syncthreads();
+    flush_hist(h, hist, 40 * M2);
+}
+
+// High-side boundary vertices (j == W, or k == D with j < W), flat.
+template <int DT, int QM>
+__global__ void __launch_bounds__(256) hist3d_edge(const typename Elem<DT>::T* __restrict__ buf, Geo3 g,
+                                                   QuantDev q, Step3 step,
+                                                   unsigned long long* __restrict__ hist)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int M2 = g.M + 2;
+    uint32_t* h = reinterpret_cast<uint32_t*>(smem_raw);
+    uint32_t* trans = h + 40 * M2;
+    float* tt = reinterpret_cast<float*>(trans + 2048);
+    init_shared3(h, trans, tt, step, q, M2, QM != FT_Q_IDENTITY);
+    __syncthreads();
+    const int64_t per_row = (g.D + 1) + g.W;
+    const int64_t n = (g.v1 - g.v0) * per_row;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = g.v0 + t / per_row;
+        const int64_t r = t % per_row;
+        int64_t j, k;
+        if (r <= g.D) {
+            j = g.W;
+            k = r;
+        } else {
+            j = r - (g.D + 1);
+            k = g.D;
+        }
+        uint32_t k8[8];
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+            k8[s] = level3<DT, QM>(buf, g, i - 1 + (s & 1), j - 1 + ((s >> 1) & 1), k - 1 + ((s >> 2) & 1),
+                                   tt, q) * 8 + s;
+        // slots 0,2,4,6 and 1,3,5,7 sorted separately, then merged
+        uint32_t a[8] = {k8[0], k8[2], k8[4], k8[6], k8[1], k8[3], k8[5], k8[7]};
+        sort4(a[0], a[1], a[2], a[3]);
+        sort4(a[4], a[5], a[6], a[7]);
+        merge44(a);
+        book3(h, trans, a, M2);
+    }
+    __syncthreads();
+    flush_hist(h, hist, 40 * M2);
+}
+
+static Step3 make_step3()
+{
+    const Tables& t = tables(3);
+    Step3 s;
+    for (int i = 0; i < 2048; ++i) s.cls[i] = t.step[i] < 0 ? 255 : (uint8_t)t.step[i];
+    return s;
+}
+
+static int sm_count()
+{
+    int dev = 0, n = kSMs;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+}
+
+template <int DT, int QM>
+static int launch3(const ft_window* win, int64_t H, int64_t W, int64_t D, int64_t v0, int64_t v1,
+                   const ft_quant* qa, int32_t M, uint64_t* hist, cudaStream_t st)
+{
+    using T = typename Elem<DT>::T;
+    static const Step3 step = make_step3();
+    const T* buf = static_cast<const T*>(win->data);
+    Geo3 g{};
+    g.H = H; g.W = W; g.D = D; g.v0 = v0; g.v1 = v1; g.first = win->first; g.M = M;
+    QuantDev q{qa ? qa->mode : FT_Q_IDENTITY, qa ? qa->negate : 0, qa ? qa->scale : 0.f,
+               qa ? qa->bias : 0.f, qa ? qa->thresholds : nullptr};
+    const int M2 = M + 2;
+    const size_t sm_hist = (size_t)(40 * M2 + 2048 + M2) * 4;
+    const size_t sm_tiled = sm_hist + 2 * PN3 * sizeof(uint16_t);
+    auto* out = reinterpret_cast<unsigned long long*>(hist);
+    const int nsm = sm_count();
+
+    if (W > 0 && D > 0) {
+        auto kern = hist3d_tiled<DT, QM>;
+        FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_tiled));
+        int per_sm = 0;
+        FT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT3, sm_tiled));
+        if (per_sm < 1) return FT_ERR_ARG;
+        g.tiles_j = (int)cdiv(W, TJ3);
+        g.tiles_k = (int)cdiv(D, TK3);
+        const int64_t tiles = (int64_t)g.tiles_j * g.tiles_k;
+        const int64_t rows = v1 - v0;
+        const int64_t grid_cap = (int64_t)nsm * per_sm;
+        // enough items to balance (>= ~8 per CTA) while keeping chunks long
+        int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>(cdiv(8 * grid_cap, tiles), rows / 32));
+        g.chunk = (int)cdiv(rows, nchunks);
+        nchunks = cdiv(rows, g.chunk);
+        g.n_items = tiles * nchunks;
+        const int grid = (int)std::min<int64_t>(grid_cap, g.n_items);
+        kern<<<grid, NT3, sm_tiled, st>>>(buf, g, q, step, out);
+        FT_CUDA_TRY(cudaGetLastError());
+    }
+    {
+        auto kern = hist3d_edge<DT, QM>;
+        FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_hist));
+        const int64_t n = (v1 - v0) * ((D + 1) + W);
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256 * 16), nsm));
+        kern<<<grid, 256, sm_hist, st>>>(buf, g, q, step, out);
+        FT_CUDA_TRY(cudaGetLastError());
+    }
+    return FT_OK;
+}
+
+}  // namespace ft
+
+using namespace ft;
+
+extern "C" int ft_hist3d(const ft_window* win, int64_t H, int64_t W, int64_t D, int64_t v0, int64_t v1,
+                         const ft_quant* q, int32_t M, uint64_t* hist, void* stream)
+{
+    if (!win || !hist || H < 1 || W < 1 || D < 1 || M < 0 || v0 < 0 || v1 > H + 1 || v0 > v1) return FT_ERR_ARG;
+    if (v0 == v1) return FT_OK;
+    // every plane a vertex row in [v0, v1) reads must be resident
+    const int64_t need_lo = std::max<int64_t>(v0 - 1, 0), need_hi = std::min<int64_t>(v1 - 1, H - 1);
+    if (need_lo <= need_hi && (win->data == nullptr || need_lo < win->first || need_hi >= win->first + win->count))
+        return FT_ERR_ARG;
+    const size_t smem = (size_t)(40 * (M + 2) + 2048 + (M + 2)) * 4 + 2 * PN3 * 2;
+    if (smem > 227 * 1024 || M + 1 > 65535) return FT_ERR_ARG;
+    const int qm = q ? q->mode : FT_Q_IDENTITY;
+    if (qm != FT_Q_IDENTITY && (!q->thresholds || win->dtype == FT_I32)) return FT_ERR_ARG;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+#define FT_DISPATCH3(DT)                                                                  \
+    switch (qm) {                                                                         \
+    case FT_Q_IDENTITY: return launch3<DT, FT_Q_IDENTITY>(win, H, W, D, v0, v1, q, M, hist, st); \
+    case FT_Q_TABLE: return launch3<DT, FT_Q_TABLE>(win, H, W, D, v0, v1, q, M, hist, st);       \
+    case FT_Q_TABLE_ROBUST: return launch3<DT, FT_Q_TABLE_ROBUST>(win, H, W, D, v0, v1, q, M, hist, st); \
+    default: return FT_ERR_ARG;                                                           \
+    }
+    switch (win->dtype) {
+    case FT_I32:
+        if (qm != FT_Q_IDENTITY) return FT_ERR_ARG;
+        return launch3<FT_I32, FT_Q_IDENTITY>(win, H, W, D, v0, v1, q, M, hist, st);
+    case FT_U8: FT_DISPATCH3(FT_U8)
+    case FT_U16: FT_DISPATCH3(FT_U16)
+    case FT_F32:
+        if (qm == FT_Q_IDENTITY) return FT_ERR_ARG;
+        if (qm == FT_Q_TABLE) return launch3<FT_F32, FT_Q_TABLE>(win, H, W, D, v0, v1, q, M, hist, st);
+        return launch3<FT_F32, FT_Q_TABLE_ROBUST>(win, H, W, D, v0, v1, q, M, hist, st);
+    }
+#undef FT_DISPATCH3
+    return FT_ERR_ARG;
+}

@@ -1,0 +1,196 @@
+"""Device driver: field residency, kernel launches, finalize.
+
+PyTorch supplies device memory, streams and ``torch.distributed`` plumbing;
+every byte of the hot path is computed by the CUDA library through the C ABI
+(``_lib``).  Histograms are int64 tensors on the device that the library
+treats as uint64 (counts never exceed 2**63).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from ._tables import TRANSITIONS_2D, TRANSITIONS_3D
+from .quant import QuantSpec, device_struct
+
+NCLASS = {2: 6, 3: 40}
+NTYPE = {2: 5, 3: 21}
+
+_TORCH_DTYPE_CODES = None
+
+
+def torch():
+    import torch as _t
+    return _t
+
+
+def _codes():
+    global _TORCH_DTYPE_CODES
+    if _TORCH_DTYPE_CODES is None:
+        t = torch()
+        _TORCH_DTYPE_CODES = {t.int32: _lib.FT_I32, t.uint8: _lib.FT_U8, t.uint16: _lib.FT_U16,
+                              t.float32: _lib.FT_F32, t.float64: _lib.FT_F64}
+    return _TORCH_DTYPE_CODES
+
+
+def dtype_code(tensor):
+    try:
+        return _codes()[tensor.dtype]
+    except KeyError:
+        raise TypeError(f"unsupported field dtype {tensor.dtype}; use int32 levels, uint8, "
+                        "uint16 or float32") from None
+
+
+def default_device(device=None):
+    t = torch()
+    if not t.cuda.is_available():
+        raise RuntimeError("fieldtopo-b200 needs a CUDA device (B200, sm_100a); none is visible")
+    if device is None:
+        return t.device("cuda", t.cuda.current_device())
+    d = t.device(device)
+    if d.type != "cuda":
+        raise ValueError(f"device must be a CUDA device, got {d}")
+    return d if d.index is not None else t.device("cuda", t.cuda.current_device())
+
+
+def _stream_ptr(device):
+    return ctypes.c_void_p(torch().cuda.current_stream(device).cuda_stream)
+
+
+def to_device(array, device, pinned=True):
+    """numpy/torch array -> contiguous CUDA tensor (pinned-staged H2D)."""
+    t = torch()
+    if isinstance(array, t.Tensor):
+        x = array
+    else:
+        a = np.ascontiguousarray(array)
+        if a.dtype == np.int64:
+            a = a.astype(np.int32)
+        x = t.from_numpy(a)
+        if pinned and x.numel() * x.element_size() >= (1 << 20):
+            x = x.pin_memory()
+    return x.to(device, non_blocking=True).contiguous()
+
+
+def new_hist(ndim, M, device, batch=1):
+    shape = (NCLASS[ndim], M + 2) if batch == 1 else (batch, NCLASS[ndim], M + 2)
+    return torch().zeros(shape, dtype=torch().int64, device=device)
+
+
+def launch_hist(ndim, x, shape, M, quant, rows=None, first=0, hist=None, batch=1, batch_stride=0):
+    """Accumulate transition histograms of vertex rows ``rows`` = [v0, v1).
+
+    ``x``: CUDA tensor holding rows/planes [first, first + count) of a field of
+    global shape ``shape`` ((H, W) or (H, W, D)); for ``batch`` > 1 (2D) the
+    images are ``batch_stride`` elements apart."""
+    L = _lib.load()
+    dev = x.device
+    H = shape[0]
+    v0, v1 = rows if rows is not None else (0, H + 1)
+    if hist is None:
+        hist = new_hist(ndim, M, dev, batch)
+    count = x.shape[1] if batch > 1 else x.shape[0]
+    win = _lib.ft_window(ctypes.c_void_p(x.data_ptr()), dtype_code(x), int(first), int(count),
+                         int(batch), int(batch_stride))
+    qs, keep = device_struct(quant, dev)
+    st = _stream_ptr(dev)
+    if ndim == 2:
+        rc = L.ft_hist2d(ctypes.byref(win), H, shape[1], v0, v1, ctypes.byref(qs), M,
+                         ctypes.c_void_p(hist.data_ptr()), st)
+    else:
+        rc = L.ft_hist3d(ctypes.byref(win), H, shape[1], shape[2], v0, v1, ctypes.byref(qs), M,
+                         ctypes.c_void_p(hist.data_ptr()), st)
+    del keep
+    _lib.check(rc, f"ft_hist{ndim}d")
+    return hist
+
+
+def class_weights(ndim, eighths):
+    tables = TRANSITIONS_3D if ndim == 3 else TRANSITIONS_2D
+    w = np.asarray(eighths, np.int64)
+    if w.shape != (tables.n_types,):
+        raise ValueError(f"{ndim}D table needs {tables.n_types} weights")
+    out = np.zeros(tables.n_classes, np.int64)
+    _lib.check(_lib.load().ft_class_weights(ndim, w.ctypes.data, out.ctypes.data), "ft_class_weights")
+    return out
+
+
+def finalize(ndim, M, hist, maps=True, tables=()):
+    """Device q_in/q_out (uint64 as int64, or None) and numerators [n_desc, M+1]."""
+    t = torch()
+    L = _lib.load()
+    dev = hist.device
+    batch = hist.shape[0] if hist.dim() == 3 else 1
+    T = NTYPE[ndim]
+    shp = (T, M + 2) if batch == 1 else (batch, T, M + 2)
+    q_in = t.empty(shp, dtype=t.int64, device=dev) if maps else None
+    q_out = t.empty(shp, dtype=t.int64, device=dev) if maps else None
+    n_desc = len(tables)
+    cw = num = None
+    if n_desc:
+        cw = t.from_numpy(np.stack([class_weights(ndim, w) for w in tables])).to(dev)
+        num = t.empty((n_desc, M + 1) if batch == 1 else (batch, n_desc, M + 1), dtype=t.int64, device=dev)
+    ptr = lambda a: ctypes.c_void_p(a.data_ptr()) if a is not None else None  # noqa: E731
+    rc = L.ft_finalize(ndim, M, batch, ptr(hist), ptr(q_in), ptr(q_out), n_desc, ptr(cw), ptr(num),
+                       _stream_ptr(dev))
+    _lib.check(rc, "ft_finalize")
+    return q_in, q_out, num
+
+
+def curves_from_maps(q_in, q_out, M, eighths_list, device):
+    """descriptor_curve / counts_at_levels on device: weighted prefix scan of
+    the rows (q_in; q_out) with weights (w; -w)."""
+    t = torch()
+    L = _lib.load()
+    rows = np.concatenate([np.asarray(q_in, np.uint64), np.asarray(q_out, np.uint64)]).view(np.int64)
+    w = np.asarray(eighths_list, np.int64)
+    row_w = np.concatenate([w, -w], axis=1)
+    r = t.from_numpy(np.ascontiguousarray(rows)).to(device)
+    rw = t.from_numpy(np.ascontiguousarray(row_w)).to(device)
+    out = t.empty((len(w), M + 1), dtype=t.int64, device=device)
+    rc = L.ft_curves(ctypes.c_void_p(r.data_ptr()), rows.shape[0], M, 1, len(w), ctypes.c_void_p(rw.data_ptr()),
+                     ctypes.c_void_p(out.data_ptr()), _stream_ptr(device))
+    _lib.check(rc, "ft_curves")
+    return out.cpu().numpy()
+
+
+def quantize_device(x, quant, M):
+    """Standalone device quantize -> int32 tensor."""
+    t = torch()
+    L = _lib.load()
+    out = t.empty(x.shape, dtype=t.int32, device=x.device)
+    qs, keep = device_struct(quant, x.device, f64=x.dtype == t.float64)
+    rc = L.ft_quantize(ctypes.c_void_p(x.data_ptr()), dtype_code(x), x.numel(), ctypes.byref(qs), M,
+                       ctypes.c_void_p(out.data_ptr()), _stream_ptr(x.device))
+    del keep
+    _lib.check(rc, "ft_quantize")
+    return out
+
+
+def minmax_device(x):
+    """(min, max) of a CUDA tensor as Python floats (device reduction)."""
+    t = torch()
+    L = _lib.load()
+    out = t.empty(4, dtype=t.int32, device=x.device)
+    code = dtype_code(x)
+    rc = L.ft_minmax(ctypes.c_void_p(x.data_ptr()), code, x.numel(), ctypes.c_void_p(out.data_ptr()),
+                     _stream_ptr(x.device))
+    _lib.check(rc, "ft_minmax")
+    raw = out.cpu().numpy()
+    if code == _lib.FT_F64:
+        k = raw.view(np.uint64)
+        return L.ft_key64_to_double(int(k[0])), L.ft_key64_to_double(int(k[1]))
+    k = raw.view(np.uint32)
+    return L.ft_key_to_double(code, int(k[0])), L.ft_key_to_double(code, int(k[1]))
+
+
+def as_uint64(t):
+    """Device int64 histogram/map tensor -> host numpy uint64."""
+    return t.cpu().numpy().view(np.uint64)
+
+
+__all__ = ["launch_hist", "finalize", "curves_from_maps", "quantize_device", "minmax_device", "to_device",
+           "default_device", "new_hist", "as_uint64", "class_weights", "QuantSpec"]
