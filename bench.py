@@ -191,23 +191,25 @@ def main():
     quant = ft.quant.QuantSpec.for_range(0.0, 1.0, M)
     tables = [ft.builtin_weights(d, "26C") for d in descs]
     eighths = [t.eighths for t in tables]
-    hist = engine.new_hist(3, M, dev)
+    row_w = np.array([ft.lattice.row_weights(3, tuple(e))[0] for e in eighths], np.int64)
+    hist = engine.new_lattice_hist(3, M, dev)
     stream = torch.cuda.current_stream(dev)
     k_start, k_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     kernel_ms = []
 
     def step(timed_kernel=False):
+        # the fused curve path: element histograms (ft_lattice3d) -> NCCL
+        # all-reduce (N > 1) -> device prefix scan into the three curves
         hist.zero_()
         if timed_kernel:
             k_start.record(stream)
-        engine.launch_hist(3, x, shape, M, quant, rows=(a, b), first=r0, hist=hist)
+        engine.launch_lattice(3, x, shape, M, quant, rows=(a, b), first=r0, hist=hist)
         if timed_kernel:
             k_end.record(stream)
         if ws > 1:
             import torch.distributed as dist
             dist.all_reduce(hist)
-        _, _, num = engine.finalize(3, M, hist, maps=False, tables=eighths)
-        return num
+        return engine.curves_from_rows(hist, M, row_w)
 
     def barrier():
         if ws > 1:
@@ -241,6 +243,18 @@ def main():
     ms, kms = t_ms.tolist()
     cells = H * W * D
     value = cells / (ms / 1e3) / 1e9
+    # the contribution-map kernel (drop-in gather_3d_*), same field, reported beside
+    mhist = engine.new_hist(3, M, dev)
+    map_ms = []
+    for _ in range(3):
+        mhist.zero_()
+        k_start.record(stream)
+        engine.launch_hist(3, x, shape, M, quant, rows=(a, b), first=r0, hist=mhist)
+        k_end.record(stream)
+        torch.cuda.synchronize()
+        map_ms.append(k_start.elapsed_time(k_end))
+    del mhist
+    map_gvox = (r1 - r0) * W * D / (statistics.median(map_ms) / 1e3) / 1e9
 
     # ---- end to end through the public API, host-resident input ----------
     e2e = None
@@ -250,20 +264,24 @@ def main():
         host.copy_(x)
         del x
         torch.cuda.empty_cache()
-        src = ft.ArraySource(host.numpy(), M, value_range=(0.0, 1.0))
-        # the rank's planes [r0, r1) stand for global planes; shift the vertex rows
-        local_src = _ShiftedSource(src, r0, H)
+        src = ft.ArraySource(host, M, value_range=(0.0, 1.0))  # pinned: H2D straight from its pages
+        lattice_kind = ft.gather.Kind("lattice")
         e_times = []
         for it in range(1 + e2e_steps):
             barrier()
             torch.cuda.synchronize()
             s = time.perf_counter()
-            h = ft.gather.stream_hist(local_src, 3, dev, (a, b), chunk_bytes=512 << 20)
-            if ws > 1:
+            if ws == 1:
+                # the public call a user makes
+                curves = np.stack([c.numerators for c in ft.descriptor_curves(src, tables, device=dev,
+                                                                              chunk_bytes=512 << 20)])
+            else:
+                # the rank's planes [r0, r1) stand for global planes
+                h = ft.gather.stream_hist(_ShiftedSource(src, r0, H), 3, dev, (a, b), chunk_bytes=512 << 20,
+                                          kind=lattice_kind)
                 import torch.distributed as dist
                 dist.all_reduce(h)
-            _, _, num = engine.finalize(3, M, h, maps=False, tables=eighths)
-            curves = num.cpu().numpy()
+                curves = engine.curves_from_rows(h, M, row_w).cpu().numpy()
             torch.cuda.synchronize()
             if it:
                 e_times.append(time.perf_counter() - s)
@@ -299,10 +317,13 @@ def main():
                "config": config,
                "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                             "frac": round(achieved / peak, 4), "traffic": None,
-                            "kernel": "hist3d_tiled (+edge), per-launch median over CUDA events",
+                            "kernel": "lattice3d_kernel (fused curve histograms), per-launch median over CUDA events",
                             "kernel_ms": round(kms, 4), "peak_source": peak_kind,
                             "algorithmic_bytes_per_launch": int(bytes_per_launch)},
-               "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": 3 * args.steps,
+               "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": 2 * args.steps,
+               "map_path": {"kernel": "hist3d_tiled + hist3d_edge (transition-class maps, gather_3d_*)",
+                            "value": round(map_gvox, 4), "unit": "Gvoxels/s",
+                            "kernel_ms": round(statistics.median(map_ms), 4)},
                "clocks": clk.summary()}
         print(json.dumps(out))
     if ws > 1:
@@ -322,6 +343,7 @@ class _ShiftedSource:
         self.height, self.width, self.depth = H, src.width, src.depth
         self.shape = (H, src.width, src.depth)
         self.peak_field_bytes = 0
+        self.pinned_rows, self.pinned_first = src.pinned_rows, r0
 
     def note_resident(self, n):
         self.peak_field_bytes = max(self.peak_field_bytes, n)

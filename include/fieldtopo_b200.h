@@ -52,7 +52,10 @@ extern "C" {
  * reference quantize_with_range(x, lo, hi, M) (fields.py:20-33), decided by
  * `thresholds` (device, M+2 floats: [-inf, t_1 .. t_M, NaN], t_l = smallest
  * float32 whose reference level is >= l) after the estimate
- * floor(fmaf(x', scale, bias)), x' = negate ? -x : x. */
+ * est = clamp(floor(fmaf(x', scale, bias)), 0, M), x' = negate ? -x : x.
+ * FT_Q_TABLE requires est in {L-1, L} (the caller checks the conditioning;
+ * bias = -lo * scale) and negate == 0: level = est + (x >= t[est+1]).  FT_Q_TABLE_ROBUST
+ * walks the table from any estimate. */
 typedef struct ft_quant {
     int32_t mode;
     int32_t negate;
@@ -91,6 +94,22 @@ int ft_hist2d(const ft_window *win, int64_t H, int64_t W, int64_t v0, int64_t v1
  * (contrib3d.py:373-414). */
 int ft_hist3d(const ft_window *win, int64_t H, int64_t W, int64_t D, int64_t v0, int64_t v1,
               const ft_quant *q, int32_t M, uint64_t *hist, void *stream);
+
+/* Fused curve path (no maps): histograms, by level, of the cells of the
+ * closed cubical complex -- an element appears at the MIN level of its
+ * incident cells (MAX level for the "all incident cells active" counts).
+ * Order-free, so no tie-breaking; every builtin descriptor_curve
+ * (descriptors.py:83-97, 169-178) is an integer combination of the rows
+ * (DESIGN.md §3b).  Lattice points cover [v0, v1) x [0, W] (x [0, D]).
+ * 3D hist: device uint64 [4][M+2] rows (cells, face mins, edge mins,
+ *   vertex mins); requires D even, (M+1)*4 <= 65535.
+ * 2D hist: device uint64 [batch][4][M+2] rows (cells, edge mins, vertex
+ *   mins, vertex maxes; the last only when maxes != 0); requires W even.
+ * Both accumulate, like ft_hist2d/3d. */
+int ft_lattice3d(const ft_window *win, int64_t H, int64_t W, int64_t D, int64_t v0, int64_t v1,
+                 const ft_quant *q, int32_t M, uint64_t *hist, void *stream);
+int ft_lattice2d(const ft_window *win, int64_t H, int64_t W, int64_t v0, int64_t v1,
+                 const ft_quant *q, int32_t M, int32_t maxes, uint64_t *hist, void *stream);
 
 /* Transition histograms -> contribution maps and descriptor curves.
  * hist [batch][C][M+2] (C = 6 or 40).  q_in / q_out (may be NULL): device

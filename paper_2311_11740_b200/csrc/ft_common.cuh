@@ -36,14 +36,15 @@ __device__ __forceinline__ T ld_stream(const T* p) { return __ldg(p); }
 // (fields.py:20-33) is monotone, so a host-built float32 threshold table
 // tt[0..M+1] (tt[0] = -inf, tt[l] = smallest x with level(x) >= l,
 // tt[M+1] = NaN) decides it exactly: level(x) = #{l >= 1 : x >= tt[l]}.
-// A float32 FMA estimate lands within +-1 of the answer for well-conditioned
-// ranges (host-checked) and one compare on each side fixes it; ill-conditioned
-// ranges use the walking variant.
+// FT_Q_TABLE: the host guarantees the float32 estimate
+// est = clamp(floor(fmaf(x, scale, bias)), 0, M) is the level L or L - 1
+// (bias = -lo * scale, estimate error < 0.5 level), so ONE comparison fixes it.
+// FT_Q_TABLE_ROBUST (ill-conditioned ranges) walks the table both ways.
 struct QuantDev {
     int mode;        // FT_Q_IDENTITY / FT_Q_TABLE / FT_Q_TABLE_ROBUST
     int negate;      // reversed range (hi < lo): evaluate on -x
     float scale, bias;
-    const float* tt; // device, M+2 entries (shared copy made by kernels)
+    const float* tt; // device, M+2 entries (kernels stage a shared copy)
 };
 
 template <int DT, int QM>
@@ -57,17 +58,34 @@ __device__ __forceinline__ uint32_t to_level(typename Elem<DT>::T raw, const flo
         return min(v, (uint32_t)(M + 1));
     } else {
         float x = (float)raw;
-        if (negate) x = -x;
+        if constexpr (QM == FT_Q_TABLE_ROBUST) {
+            if (negate) x = -x;  // FT_Q_TABLE is never used for reversed ranges
+        }
         int est = __float2int_rd(fmaf(x, scale, bias));
         est = min(max(est, 0), M);
         if constexpr (QM == FT_Q_TABLE) {
             est += (x >= tt[est + 1]) ? 1 : 0;
-            est -= (x < tt[est]) ? 1 : 0;
         } else {
             while (est < M && x >= tt[est + 1]) ++est;
             while (est > 0 && x < tt[est]) --est;
         }
         return (uint32_t)est;
+    }
+}
+
+// level * 4 (a shared-memory byte offset), for the 16-bit packed kernels.
+template <int DT, int QM>
+__device__ __forceinline__ uint32_t to_level4(typename Elem<DT>::T raw, const float* __restrict__ tt, float scale,
+                                              float bias, int negate, int M)
+{
+    if constexpr (QM == FT_Q_TABLE) {
+        const float x = (float)raw;
+        const int est = min(max(__float2int_rd(fmaf(x, scale, bias)), 0), M);
+        const uint32_t e4 = (uint32_t)est << 2;
+        const float t = *reinterpret_cast<const float*>(reinterpret_cast<const char*>(tt) + e4 + 4);
+        return x >= t ? e4 + 4 : e4;
+    } else {
+        return to_level<DT, QM>(raw, tt, scale, bias, negate, M) << 2;
     }
 }
 
@@ -81,7 +99,6 @@ __device__ __forceinline__ uint32_t to_level_f64(double x, const double* __restr
     int est = (y != y) ? 0 : (y <= 0.0 ? 0 : (y >= (double)M ? M : (int)floor(y)));
     if constexpr (QM == FT_Q_TABLE) {
         est += (x >= tt[est + 1]) ? 1 : 0;
-        est -= (x < tt[est]) ? 1 : 0;
     } else {
         while (est < M && x >= tt[est + 1]) ++est;
         while (est > 0 && x < tt[est]) --est;
@@ -128,6 +145,13 @@ __device__ __forceinline__ void merge22(uint32_t& a, uint32_t& b, uint32_t& c, u
     cswap(a, c);
     cswap(b, d);
     cswap(b, c);
+}
+
+// FT_Q_TABLE assumes an increasing range; reversed ranges take the walking path.
+inline int effective_qmode(const ft_quant* q)
+{
+    if (!q) return FT_Q_IDENTITY;
+    return (q->mode == FT_Q_TABLE && q->negate) ? FT_Q_TABLE_ROBUST : q->mode;
 }
 
 __host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -216,31 +216,32 @@ extern "C" int ft_quantize(const void* x, int32_t dtype, int64_t n, const ft_qua
     if (!x) return FT_ERR_ARG;
     if (q->mode != FT_Q_IDENTITY && !q->thresholds) return FT_ERR_ARG;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    QuantDev qd{q->mode, q->negate, q->scale, q->bias, q->thresholds};
+    const int qmode = effective_qmode(q);
+    QuantDev qd{qmode, q->negate, q->scale, q->bias, q->thresholds};
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 16 * nsm()));
 #define FT_Q_LAUNCH(DT, QM) \
     quantize_kernel<DT, QM><<<grid, 256, 0, st>>>(static_cast<const typename Elem<DT>::T*>(x), n, qd, M, out)
     switch (dtype) {
     case FT_U8:
-        if (q->mode == FT_Q_IDENTITY) FT_Q_LAUNCH(FT_U8, FT_Q_IDENTITY);
-        else if (q->mode == FT_Q_TABLE) FT_Q_LAUNCH(FT_U8, FT_Q_TABLE);
+        if (qmode == FT_Q_IDENTITY) FT_Q_LAUNCH(FT_U8, FT_Q_IDENTITY);
+        else if (qmode == FT_Q_TABLE) FT_Q_LAUNCH(FT_U8, FT_Q_TABLE);
         else FT_Q_LAUNCH(FT_U8, FT_Q_TABLE_ROBUST);
         break;
     case FT_U16:
-        if (q->mode == FT_Q_IDENTITY) FT_Q_LAUNCH(FT_U16, FT_Q_IDENTITY);
-        else if (q->mode == FT_Q_TABLE) FT_Q_LAUNCH(FT_U16, FT_Q_TABLE);
+        if (qmode == FT_Q_IDENTITY) FT_Q_LAUNCH(FT_U16, FT_Q_IDENTITY);
+        else if (qmode == FT_Q_TABLE) FT_Q_LAUNCH(FT_U16, FT_Q_TABLE);
         else FT_Q_LAUNCH(FT_U16, FT_Q_TABLE_ROBUST);
         break;
     case FT_F32:
-        if (q->mode == FT_Q_IDENTITY) return FT_ERR_ARG;
-        if (q->mode == FT_Q_TABLE) FT_Q_LAUNCH(FT_F32, FT_Q_TABLE);
+        if (qmode == FT_Q_IDENTITY) return FT_ERR_ARG;
+        if (qmode == FT_Q_TABLE) FT_Q_LAUNCH(FT_F32, FT_Q_TABLE);
         else FT_Q_LAUNCH(FT_F32, FT_Q_TABLE_ROBUST);
         break;
     case FT_F64:
         // scale / bias travel as float in ft_quant; the double estimate only
         // needs to land within +-1 level (host-checked), the table decides.
-        if (q->mode == FT_Q_IDENTITY) return FT_ERR_ARG;
-        if (q->mode == FT_Q_TABLE)
+        if (qmode == FT_Q_IDENTITY) return FT_ERR_ARG;
+        if (qmode == FT_Q_TABLE)
             quantize_f64_kernel<FT_Q_TABLE><<<grid, 256, 0, st>>>(static_cast<const double*>(x), n, qd, M, out);
         else
             quantize_f64_kernel<FT_Q_TABLE_ROBUST><<<grid, 256, 0, st>>>(static_cast<const double*>(x), n, qd, M, out);

@@ -247,7 +247,7 @@ extern "C" int ft_hist2d(const ft_window* win, int64_t H, int64_t W, int64_t v0,
         return FT_ERR_ARG;
     const size_t smem = (size_t)(FT_NCLASS_2D * (M + 2) + (M + 2)) * 4 + 2 * RW2 * 2;
     if (smem > 227 * 1024 || M + 1 > 65535) return FT_ERR_ARG;
-    const int qm = q ? q->mode : FT_Q_IDENTITY;
+    const int qm = effective_qmode(q);
     if (qm != FT_Q_IDENTITY && !q->thresholds) return FT_ERR_ARG;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     switch (win->dtype) {

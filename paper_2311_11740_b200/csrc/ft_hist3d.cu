@@ -7,29 +7,33 @@
 // exactly (ties resolve by slot).  Each sorted rank books ONE event into a
 // per-CTA shared-memory histogram keyed by the transition class
 // (type_n -> type_{n+1}, 40 classes) instead of the reference's
-// 15 q_in/q_out increments.
+// 15 q_in/q_out increments.  The classes of ranks 1-3 are a function of the
+// first four sorted slots and those of ranks 4-6 of the last four, so two
+// 4096-entry shared tables (one lookup each) classify all six middle ranks.
 //
-// Tiling: a CTA owns a TJ x TK tile of vertex columns (j, k)
-// and marches vertex rows i (the slowest, slab axis).  Each step stages one
-// cell plane tile (+1-cell low halo) into shared memory as 16-bit levels,
-// quantizing on the fly; the plane below stays in registers as an
-// already-sorted 4-key list, so each vertex sorts 4 new keys (5 compare-
-// exchanges) and merges (9) instead of sorting 8 (19).  Global loads run two
-// planes ahead of the compute.  Vertex columns j == W or k == D (the
+// Tiling: a 1024-thread CTA owns a 32 x 32 tile of vertex
+// columns (j, k) and marches vertex rows i (the slowest, slab axis).  Each
+// step stages one cell-plane tile (+1-cell low halo) into shared memory as
+// 16-bit levels, quantizing on the fly; the plane below stays in registers
+// as an already-sorted 4-key list, so a vertex sorts 4 new keys (5
+// compare-exchanges) and merges (9) instead of sorting 8 (19).  Global loads
+// run two planes ahead of the compute; tile addressing is 32-bit with the
+// per-tile bounds folded into a validity bit, so the per-plane cost is one
+// uniform 64-bit pointer bump.  Vertex columns j == W or k == D (the
 // high-side boundary) are done by a flat per-vertex kernel.
 #include <algorithm>
-#include <mutex>
 
 #include "ft_common.cuh"
 #include "ft_tables.h"
 
 namespace ft {
 
-constexpr int TJ3 = 8, TK3 = 32, NT3 = TJ3 * TK3;
-constexpr int PW3 = TK3 + 1;          // staged plane tile row pitch
-constexpr int PN3 = (TJ3 + 1) * PW3;  // staged cells per plane (297)
+constexpr int TJ3 = 32, TK3 = 32, NT3 = TJ3 * TK3;
+constexpr int PW3 = TK3 + 1;          // staged plane tile row pitch (33)
+constexpr int PN3 = (TJ3 + 1) * PW3;  // staged cells per plane (1089)
 constexpr int LD3 = (PN3 + NT3 - 1) / NT3;
 constexpr int PF3 = 2;                // planes in flight
+constexpr int NTAB = 4096;            // rank-group table entries
 
 struct Geo3 {
     int64_t H, W, D, v0, v1, first;
@@ -38,37 +42,51 @@ struct Geo3 {
     int64_t n_items;
 };
 
+// Class ids of ranks (1,2,3) indexed by the first four sorted slots, and of
+// ranks (4,5,6) by the last four (bytes 0..2 of each entry).
+struct RankTables {
+    uint32_t a[NTAB];
+    uint32_t b[NTAB];
+};
+
 template <int DT, int QM>
-__device__ __forceinline__ uint32_t level3(const typename Elem<DT>::T* __restrict__ buf,
-                                           const Geo3& g, int64_t p, int64_t j, int64_t k,
-                                           const float* tt, const QuantDev& q)
+__device__ __forceinline__ uint32_t level3(const typename Elem<DT>::T* __restrict__ buf, const Geo3& g,
+                                           int64_t p, int64_t j, int64_t k, const float* tt, const QuantDev& q)
 {
     if (p < 0 || p >= g.H || j < 0 || j >= g.W || k < 0 || k >= g.D) return (uint32_t)g.M + 1;
-    return to_level<DT, QM>(ld_stream(buf + ((p - g.first) * g.W + j) * g.D + k), tt, q.scale,
-                            q.bias, q.negate, g.M);
+    return to_level<DT, QM>(ld_stream(buf + ((p - g.first) * g.W + j) * g.D + k), tt, q.scale, q.bias,
+                            q.negate, g.M);
 }
 
-__device__ __forceinline__ void book3(uint32_t* __restrict__ h, const uint32_t* __restrict__ trans,
-                                      const uint32_t (&k8)[8], int M2)
+__device__ __forceinline__ uint32_t slot_index(uint32_t a, uint32_t b, uint32_t c, uint32_t d)
 {
-    atomicAdd(&h[k8[0] >> 3], 1u);
-    uint32_t mask = 1u << (k8[0] & 7);
-#pragma unroll
-    for (int r = 1; r < 7; ++r) {
-        const uint32_t s = k8[r] & 7;
-        atomicAdd(&h[trans[(mask << 3) | s] + (k8[r] >> 3)], 1u);
-        mask |= 1u << s;
-    }
-    atomicAdd(&h[39 * M2 + (k8[7] >> 3)], 1u);
+    return ((a & 7u) << 9) | ((b & 7u) << 6) | ((c & 7u) << 3) | (d & 7u);
 }
 
-__device__ __forceinline__ void init_shared3(uint32_t* h, uint32_t* trans, float* tt, const Step3& step,
-                                             const QuantDev& q, int M2, bool table)
+// Book the 8 events of one vertex (k8 sorted ascending).
+__device__ __forceinline__ void book3(uint32_t* __restrict__ h, const uint32_t* __restrict__ ta,
+                                      const uint32_t* __restrict__ tb, const uint32_t (&k8)[8], uint32_t M2)
+{
+    const uint32_t ea = ta[slot_index(k8[0], k8[1], k8[2], k8[3])];
+    const uint32_t eb = tb[slot_index(k8[4], k8[5], k8[6], k8[7])];
+    atomicAdd(&h[k8[0] >> 3], 1u);
+    atomicAdd(&h[(ea & 0xFFu) * M2 + (k8[1] >> 3)], 1u);
+    atomicAdd(&h[((ea >> 8) & 0xFFu) * M2 + (k8[2] >> 3)], 1u);
+    atomicAdd(&h[(ea >> 16) * M2 + (k8[3] >> 3)], 1u);
+    atomicAdd(&h[(eb & 0xFFu) * M2 + (k8[4] >> 3)], 1u);
+    atomicAdd(&h[((eb >> 8) & 0xFFu) * M2 + (k8[5] >> 3)], 1u);
+    atomicAdd(&h[(eb >> 16) * M2 + (k8[6] >> 3)], 1u);
+    atomicAdd(&h[39u * M2 + (k8[7] >> 3)], 1u);
+}
+
+__device__ __forceinline__ void init_shared3(uint32_t* h, uint32_t* ta, uint32_t* tb, float* tt,
+                                             const RankTables* __restrict__ rt, const QuantDev& q, int M2,
+                                             bool table)
 {
     for (int i = threadIdx.x; i < 40 * M2; i += blockDim.x) h[i] = 0;
-    for (int i = threadIdx.x; i < 2048; i += blockDim.x) {
-        uint32_t c = step.cls[i];
-        trans[i] = c == 255 ? 0u : c * (uint32_t)M2;
+    for (int i = threadIdx.x; i < NTAB; i += blockDim.x) {
+        ta[i] = rt->a[i];
+        tb[i] = rt->b[i];
     }
     if (table)
         for (int i = threadIdx.x; i < M2; i += blockDim.x) tt[i] = q.tt[i];
@@ -83,18 +101,19 @@ __device__ __forceinline__ void flush_hist(const uint32_t* h, unsigned long long
 }
 
 template <int DT, int QM>
-__global__ void __launch_bounds__(NT3) hist3d_tiled(const typename Elem<DT>::T* __restrict__ buf,
-                                                    Geo3 g, QuantDev q, Step3 step,
-                                                    unsigned long long* __restrict__ hist)
+__global__ void __launch_bounds__(NT3, 1) hist3d_tiled(const typename Elem<DT>::T* __restrict__ buf, Geo3 g,
+                                                       QuantDev q, const RankTables* __restrict__ rt,
+                                                       unsigned long long* __restrict__ hist)
 {
     using T = typename Elem<DT>::T;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int M2 = g.M + 2;
     uint32_t* h = reinterpret_cast<uint32_t*>(smem_raw);
-    uint32_t* trans = h + 40 * M2;
-    float* tt = reinterpret_cast<float*>(trans + 2048);
+    uint32_t* ta = h + 40 * M2;
+    uint32_t* tb = ta + NTAB;
+    float* tt = reinterpret_cast<float*>(tb + NTAB);
     uint16_t* pl = reinterpret_cast<uint16_t*>(tt + M2);
-    init_shared3(h, trans, tt, step, q, M2, QM != FT_Q_IDENTITY);
+    init_shared3(h, ta, tb, tt, rt, q, M2, QM != FT_Q_IDENTITY);
     __syncthreads();
 
     const int tid = threadIdx.x;
@@ -103,12 +122,13 @@ __global__ void __launch_bounds__(NT3) hist3d_tiled(const typename Elem<DT>::T* 
     const int64_t it0 = g.n_items * blockIdx.x / gridDim.x;
     const int64_t it1 = g.n_items * (blockIdx.x + 1) / gridDim.x;
     const uint32_t sentinel = (uint32_t)g.M + 1;
+    const int64_t plane_elems = g.W * g.D;
+    const int Wi = (int)g.W, Di = (int)g.D;
 
-    // staged-cell coordinates of this thread's loads (fixed per tile)
     int lr[LD3], lc[LD3];
 #pragma unroll
     for (int e = 0; e < LD3; ++e) {
-        int idx = tid + e * NT3;
+        const int idx = tid + e * NT3;
         lr[e] = idx / PW3;
         lc[e] = idx % PW3;
     }
@@ -116,35 +136,40 @@ __global__ void __launch_bounds__(NT3) hist3d_tiled(const typename Elem<DT>::T* 
     for (int64_t item = it0; item < it1; ++item) {
         const int64_t ch = item / per_chunk;
         const int rem = (int)(item - ch * per_chunk);
-        const int64_t j0 = (int64_t)(rem / g.tiles_k) * TJ3;
-        const int64_t k0 = (int64_t)(rem % g.tiles_k) * TK3;
+        const int j0 = (rem / g.tiles_k) * TJ3;
+        const int k0 = (rem % g.tiles_k) * TK3;
         const int64_t ia = g.v0 + ch * g.chunk;
         const int64_t ib = min(ia + (int64_t)g.chunk, g.v1);
-        const bool active = (j0 + ty < g.W) && (k0 + tx < g.D);
+        const bool active = (j0 + ty < Wi) && (k0 + tx < Di);
 
-        // Raw-value prefetch ring: lv[s] holds the RAW elements of a plane
-        // PF3 - s + 1 steps ahead; levels are produced only when a plane is
-        // stored to shared memory, so the loads stay in flight across steps.
+        // per-tile load slots: in-plane offset + validity (fixed over the march)
+        int off[LD3];
+        bool ok[LD3];
+#pragma unroll
+        for (int e = 0; e < LD3; ++e) {
+            const int jj = j0 - 1 + lr[e], kk = k0 - 1 + lc[e];
+            ok[e] = (tid + e * NT3 < PN3) && jj >= 0 && jj < Wi && kk >= 0 && kk < Di;
+            off[e] = ok[e] ? jj * Di + kk : 0;
+        }
         T lv[PF3 + 1][LD3];
-        auto inside = [&](int64_t p, int e) {
-            const int64_t jj = j0 - 1 + lr[e], kk = k0 - 1 + lc[e];
-            return (tid + e * NT3 < PN3) && p >= 0 && p < g.H && jj >= 0 && jj < g.W && kk >= 0 && kk < g.D;
-        };
         auto fetch = [&](int64_t p, T (&dst)[LD3]) {
+            const bool pin = p >= 0 && p < g.H;
+            const T* base = buf + (pin ? (p - g.first) * plane_elems : 0);
 #pragma unroll
             for (int e = 0; e < LD3; ++e) {
                 dst[e] = T(0);
-                if (inside(p, e))
-                    dst[e] = ld_stream(buf + ((p - g.first) * g.W + (j0 - 1 + lr[e])) * g.D + (k0 - 1 + lc[e]));
+                if (pin && ok[e]) dst[e] = ld_stream(base + off[e]);
             }
         };
         auto store = [&](int64_t p, uint16_t* dstp, const T (&src)[LD3]) {
+            const bool pin = p >= 0 && p < g.H;
 #pragma unroll
             for (int e = 0; e < LD3; ++e) {
                 const int idx = tid + e * NT3;
                 if (idx < PN3)
-                    dstp[idx] = (uint16_t)(inside(p, e) ? to_level<DT, QM>(src[e], tt, q.scale, q.bias, q.negate, g.M)
-                                                        : sentinel);
+                    dstp[idx] = (uint16_t)((pin && ok[e])
+                                               ? to_level<DT, QM>(src[e], tt, q.scale, q.bias, q.negate, g.M)
+                                               : sentinel);
             }
         };
         fetch(ia - 1, lv[0]);
@@ -153,10 +178,11 @@ __global__ void __launch_bounds__(NT3) hist3d_tiled(const typename Elem<DT>::T* 
         store(ia - 1, pl, lv[0]);
         __syncthreads();
 
-        uint32_t lo0 = (uint32_t)pl[ty * PW3 + tx] * 8 + 0;
-        uint32_t lo1 = (uint32_t)pl[(ty + 1) * PW3 + tx] * 8 + 2;
-        uint32_t lo2 = (uint32_t)pl[ty * PW3 + tx + 1] * 8 + 4;
-        uint32_t lo3 = (uint32_t)pl[(ty + 1) * PW3 + tx + 1] * 8 + 6;
+        const int c00 = ty * PW3 + tx;
+        uint32_t lo0 = (uint32_t)pl[c00] * 8 + 0;
+        uint32_t lo1 = (uint32_t)pl[c00 + PW3] * 8 + 2;
+        uint32_t lo2 = (uint32_t)pl[c00 + 1] * 8 + 4;
+        uint32_t lo3 = (uint32_t)pl[c00 + PW3 + 1] * 8 + 6;
         sort4(lo0, lo1, lo2, lo3);
 
         for (int64_t i = ia; i < ib; ++i) {
@@ -168,15 +194,15 @@ __global__ void __launch_bounds__(NT3) hist3d_tiled(const typename Elem<DT>::T* 
                 for (int e = 0; e < LD3; ++e) lv[s][e] = lv[s + 1][e];
             if (i + PF3 < ib) fetch(i + PF3, lv[PF3]);
             __syncthreads();
-            uint32_t u0 = (uint32_t)cur[ty * PW3 + tx] * 8 + 1;
-            uint32_t u1 = (uint32_t)cur[(ty + 1) * PW3 + tx] * 8 + 3;
-            uint32_t u2 = (uint32_t)cur[ty * PW3 + tx + 1] * 8 + 5;
-            uint32_t u3 = (uint32_t)cur[(ty + 1) * PW3 + tx + 1] * 8 + 7;
+            uint32_t u0 = (uint32_t)cur[c00] * 8 + 1;
+            uint32_t u1 = (uint32_t)cur[c00 + PW3] * 8 + 3;
+            uint32_t u2 = (uint32_t)cur[c00 + 1] * 8 + 5;
+            uint32_t u3 = (uint32_t)cur[c00 + PW3 + 1] * 8 + 7;
             sort4(u0, u1, u2, u3);
             if (active) {
                 uint32_t k8[8] = {lo0, lo1, lo2, lo3, u0, u1, u2, u3};
                 merge44(k8);
-                book3(h, trans, k8, M2);
+                book3(h, ta, tb, k8, (uint32_t)M2);
             }
             lo0 = u0 - 1;
             lo1 = u1 - 1;
@@ -192,52 +218,70 @@ __global__ void __launch_bounds__(NT3) hist3d_tiled(const typename Elem<DT>::T* 
 // High-side boundary vertices (j == W, or k == D with j < W), flat.
 template <int DT, int QM>
 __global__ void __launch_bounds__(256) hist3d_edge(const typename Elem<DT>::T* __restrict__ buf, Geo3 g,
-                                                   QuantDev q, Step3 step,
+                                                   QuantDev q, const RankTables* __restrict__ rt,
                                                    unsigned long long* __restrict__ hist)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int M2 = g.M + 2;
     uint32_t* h = reinterpret_cast<uint32_t*>(smem_raw);
-    uint32_t* trans = h + 40 * M2;
-    float* tt = reinterpret_cast<float*>(trans + 2048);
-    init_shared3(h, trans, tt, step, q, M2, QM != FT_Q_IDENTITY);
+    uint32_t* ta = h + 40 * M2;
+    uint32_t* tb = ta + NTAB;
+    float* tt = reinterpret_cast<float*>(tb + NTAB);
+    init_shared3(h, ta, tb, tt, rt, q, M2, QM != FT_Q_IDENTITY);
     __syncthreads();
     const int64_t per_row = (g.D + 1) + g.W;
     const int64_t n = (g.v1 - g.v0) * per_row;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
-         t += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = g.v0 + t / per_row;
         const int64_t r = t % per_row;
-        int64_t j, k;
-        if (r <= g.D) {
-            j = g.W;
-            k = r;
-        } else {
-            j = r - (g.D + 1);
-            k = g.D;
-        }
+        const int64_t j = r <= g.D ? g.W : r - (g.D + 1);
+        const int64_t k = r <= g.D ? r : g.D;
         uint32_t k8[8];
 #pragma unroll
         for (int s = 0; s < 8; ++s)
-            k8[s] = level3<DT, QM>(buf, g, i - 1 + (s & 1), j - 1 + ((s >> 1) & 1), k - 1 + ((s >> 2) & 1),
-                                   tt, q) * 8 + s;
-        // slots 0,2,4,6 and 1,3,5,7 sorted separately, then merged
+            k8[s] = level3<DT, QM>(buf, g, i - 1 + (s & 1), j - 1 + ((s >> 1) & 1), k - 1 + ((s >> 2) & 1), tt, q) *
+                        8 + s;
         uint32_t a[8] = {k8[0], k8[2], k8[4], k8[6], k8[1], k8[3], k8[5], k8[7]};
         sort4(a[0], a[1], a[2], a[3]);
         sort4(a[4], a[5], a[6], a[7]);
         merge44(a);
-        book3(h, trans, a, M2);
+        book3(h, ta, tb, a, (uint32_t)M2);
     }
     __syncthreads();
     flush_hist(h, hist, 40 * M2);
 }
 
-static Step3 make_step3()
+// Rank-group tables from the step table: simulate the active-slot masks of
+// every ordered slot 4-tuple.
+static RankTables make_rank_tables()
 {
     const Tables& t = tables(3);
-    Step3 s;
-    for (int i = 0; i < 2048; ++i) s.cls[i] = t.step[i] < 0 ? 255 : (uint8_t)t.step[i];
-    return s;
+    RankTables rt{};
+    for (int idx = 0; idx < NTAB; ++idx) {
+        const int s[4] = {idx >> 9 & 7, idx >> 6 & 7, idx >> 3 & 7, idx & 7};
+        bool distinct = true;
+        for (int x = 0; x < 4; ++x)
+            for (int y = x + 1; y < 4; ++y) distinct &= s[x] != s[y];
+        if (!distinct) continue;
+        // ranks 1..3: masks {s0}, {s0,s1}, {s0,s1,s2}
+        int m = 1 << s[0];
+        uint32_t ea = 0;
+        for (int r = 1; r <= 3; ++r) {
+            ea |= (uint32_t)t.step[m * 8 + s[r]] << (8 * (r - 1));
+            m |= 1 << s[r];
+        }
+        rt.a[idx] = ea;
+        // ranks 4..6 given sorted slots s4..s7 = s[0..3]: before rank 4 the
+        // active set is the complement of {s4..s7}
+        int mb = 0xFF & ~((1 << s[0]) | (1 << s[1]) | (1 << s[2]) | (1 << s[3]));
+        uint32_t eb = 0;
+        for (int r = 0; r < 3; ++r) {
+            eb |= (uint32_t)t.step[mb * 8 + s[r]] << (8 * r);
+            mb |= 1 << s[r];
+        }
+        rt.b[idx] = eb;
+    }
+    return rt;
 }
 
 static int sm_count()
@@ -247,20 +291,39 @@ static int sm_count()
     return n;
 }
 
+// Per-device copy of the rank tables (uploaded once).
+static const RankTables* device_rank_tables()
+{
+    static const RankTables host = make_rank_tables();
+    static RankTables* dev_tabs[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    if (!dev_tabs[dev]) {
+        RankTables* p = nullptr;
+        if (cudaMalloc(&p, sizeof(RankTables)) != cudaSuccess) return nullptr;
+        if (cudaMemcpy(p, &host, sizeof(RankTables), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+        dev_tabs[dev] = p;
+    }
+    return dev_tabs[dev];
+}
+
+size_t hist3d_smem(int M) { return (size_t)(40 * (M + 2) + 2 * NTAB + (M + 2)) * 4 + 2 * PN3 * 2; }
+
 template <int DT, int QM>
 static int launch3(const ft_window* win, int64_t H, int64_t W, int64_t D, int64_t v0, int64_t v1,
                    const ft_quant* qa, int32_t M, uint64_t* hist, cudaStream_t st)
 {
     using T = typename Elem<DT>::T;
-    static const Step3 step = make_step3();
+    const RankTables* rt = device_rank_tables();
+    if (!rt) return FT_ERR_CUDA_BASE + (int)cudaErrorMemoryAllocation;
     const T* buf = static_cast<const T*>(win->data);
     Geo3 g{};
     g.H = H; g.W = W; g.D = D; g.v0 = v0; g.v1 = v1; g.first = win->first; g.M = M;
-    QuantDev q{qa ? qa->mode : FT_Q_IDENTITY, qa ? qa->negate : 0, qa ? qa->scale : 0.f,
-               qa ? qa->bias : 0.f, qa ? qa->thresholds : nullptr};
+    QuantDev q{qa ? qa->mode : FT_Q_IDENTITY, qa ? qa->negate : 0, qa ? qa->scale : 0.f, qa ? qa->bias : 0.f,
+               qa ? qa->thresholds : nullptr};
     const int M2 = M + 2;
-    const size_t sm_hist = (size_t)(40 * M2 + 2048 + M2) * 4;
-    const size_t sm_tiled = sm_hist + 2 * PN3 * sizeof(uint16_t);
+    const size_t sm_edge = (size_t)(40 * M2 + 2 * NTAB + M2) * 4;
+    const size_t sm_tiled = hist3d_smem(M);
     auto* out = reinterpret_cast<unsigned long long*>(hist);
     const int nsm = sm_count();
 
@@ -275,21 +338,21 @@ static int launch3(const ft_window* win, int64_t H, int64_t W, int64_t D, int64_
         const int64_t tiles = (int64_t)g.tiles_j * g.tiles_k;
         const int64_t rows = v1 - v0;
         const int64_t grid_cap = (int64_t)nsm * per_sm;
-        // enough items to balance (>= ~8 per CTA) while keeping chunks long
+        // enough items to balance (>= ~8 per CTA) while keeping marches long
         int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>(cdiv(8 * grid_cap, tiles), rows / 32));
         g.chunk = (int)cdiv(rows, nchunks);
         nchunks = cdiv(rows, g.chunk);
         g.n_items = tiles * nchunks;
         const int grid = (int)std::min<int64_t>(grid_cap, g.n_items);
-        kern<<<grid, NT3, sm_tiled, st>>>(buf, g, q, step, out);
+        kern<<<grid, NT3, sm_tiled, st>>>(buf, g, q, rt, out);
         FT_CUDA_TRY(cudaGetLastError());
     }
     {
         auto kern = hist3d_edge<DT, QM>;
-        FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_hist));
+        FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_edge));
         const int64_t n = (v1 - v0) * ((D + 1) + W);
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256 * 16), nsm));
-        kern<<<grid, 256, sm_hist, st>>>(buf, g, q, step, out);
+        kern<<<grid, 256, sm_edge, st>>>(buf, g, q, rt, out);
         FT_CUDA_TRY(cudaGetLastError());
     }
     return FT_OK;
@@ -303,34 +366,32 @@ extern "C" int ft_hist3d(const ft_window* win, int64_t H, int64_t W, int64_t D, 
                          const ft_quant* q, int32_t M, uint64_t* hist, void* stream)
 {
     if (!win || !hist || H < 1 || W < 1 || D < 1 || M < 0 || v0 < 0 || v1 > H + 1 || v0 > v1) return FT_ERR_ARG;
+    if (W * D > INT32_MAX / 2) return FT_ERR_ARG;  // 32-bit in-plane offsets
     if (v0 == v1) return FT_OK;
     // every plane a vertex row in [v0, v1) reads must be resident
     const int64_t need_lo = std::max<int64_t>(v0 - 1, 0), need_hi = std::min<int64_t>(v1 - 1, H - 1);
     if (need_lo <= need_hi && (win->data == nullptr || need_lo < win->first || need_hi >= win->first + win->count))
         return FT_ERR_ARG;
-    const size_t smem = (size_t)(40 * (M + 2) + 2048 + (M + 2)) * 4 + 2 * PN3 * 2;
-    if (smem > 227 * 1024 || M + 1 > 65535) return FT_ERR_ARG;
-    const int qm = q ? q->mode : FT_Q_IDENTITY;
+    if (hist3d_smem(M) > 227 * 1024 || M + 1 > 8190) return FT_ERR_ARG;
+    const int qm = effective_qmode(q);
     if (qm != FT_Q_IDENTITY && (!q->thresholds || win->dtype == FT_I32)) return FT_ERR_ARG;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-#define FT_DISPATCH3(DT)                                                                  \
-    switch (qm) {                                                                         \
-    case FT_Q_IDENTITY: return launch3<DT, FT_Q_IDENTITY>(win, H, W, D, v0, v1, q, M, hist, st); \
-    case FT_Q_TABLE: return launch3<DT, FT_Q_TABLE>(win, H, W, D, v0, v1, q, M, hist, st);       \
-    case FT_Q_TABLE_ROBUST: return launch3<DT, FT_Q_TABLE_ROBUST>(win, H, W, D, v0, v1, q, M, hist, st); \
-    default: return FT_ERR_ARG;                                                           \
-    }
     switch (win->dtype) {
     case FT_I32:
         if (qm != FT_Q_IDENTITY) return FT_ERR_ARG;
         return launch3<FT_I32, FT_Q_IDENTITY>(win, H, W, D, v0, v1, q, M, hist, st);
-    case FT_U8: FT_DISPATCH3(FT_U8)
-    case FT_U16: FT_DISPATCH3(FT_U16)
+    case FT_U8:
+        if (qm == FT_Q_IDENTITY) return launch3<FT_U8, FT_Q_IDENTITY>(win, H, W, D, v0, v1, q, M, hist, st);
+        if (qm == FT_Q_TABLE) return launch3<FT_U8, FT_Q_TABLE>(win, H, W, D, v0, v1, q, M, hist, st);
+        return launch3<FT_U8, FT_Q_TABLE_ROBUST>(win, H, W, D, v0, v1, q, M, hist, st);
+    case FT_U16:
+        if (qm == FT_Q_IDENTITY) return launch3<FT_U16, FT_Q_IDENTITY>(win, H, W, D, v0, v1, q, M, hist, st);
+        if (qm == FT_Q_TABLE) return launch3<FT_U16, FT_Q_TABLE>(win, H, W, D, v0, v1, q, M, hist, st);
+        return launch3<FT_U16, FT_Q_TABLE_ROBUST>(win, H, W, D, v0, v1, q, M, hist, st);
     case FT_F32:
         if (qm == FT_Q_IDENTITY) return FT_ERR_ARG;
         if (qm == FT_Q_TABLE) return launch3<FT_F32, FT_Q_TABLE>(win, H, W, D, v0, v1, q, M, hist, st);
         return launch3<FT_F32, FT_Q_TABLE_ROBUST>(win, H, W, D, v0, v1, q, M, hist, st);
     }
-#undef FT_DISPATCH3
     return FT_ERR_ARG;
 }

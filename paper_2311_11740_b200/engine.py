@@ -108,6 +108,60 @@ def launch_hist(ndim, x, shape, M, quant, rows=None, first=0, hist=None, batch=1
     return hist
 
 
+def new_lattice_hist(ndim, M, device, batch=1):
+    shape = (4, M + 2) if batch == 1 else (batch, 4, M + 2)
+    return torch().zeros(shape, dtype=torch().int64, device=device)
+
+
+def launch_lattice(ndim, x, shape, M, quant, rows=None, first=0, hist=None, batch=1, batch_stride=0,
+                   maxes=False):
+    """Accumulate the fused-curve element histograms (ft_lattice2d/3d) of
+    lattice rows ``rows`` = [v0, v1); arguments as ``launch_hist``."""
+    L = _lib.load()
+    dev = x.device
+    H = shape[0]
+    v0, v1 = rows if rows is not None else (0, H + 1)
+    if hist is None:
+        hist = new_lattice_hist(ndim, M, dev, batch)
+    count = x.shape[1] if batch > 1 else x.shape[0]
+    win = _lib.ft_window(ctypes.c_void_p(x.data_ptr()), dtype_code(x), int(first), int(count),
+                         int(batch), int(batch_stride))
+    qs, keep = device_struct(quant, dev)
+    st = _stream_ptr(dev)
+    if ndim == 2:
+        rc = L.ft_lattice2d(ctypes.byref(win), H, shape[1], v0, v1, ctypes.byref(qs), M, int(maxes),
+                            ctypes.c_void_p(hist.data_ptr()), st)
+    else:
+        rc = L.ft_lattice3d(ctypes.byref(win), H, shape[1], shape[2], v0, v1, ctypes.byref(qs), M,
+                            ctypes.c_void_p(hist.data_ptr()), st)
+    del keep
+    _lib.check(rc, f"ft_lattice{ndim}d")
+    return hist
+
+
+def lattice_ok(ndim, shape, M, x=None):
+    """Whether the fused lattice kernels accept this field (levels * 4 must
+    fit the 16-bit packed lanes)."""
+    return (M + 1) * 4 <= 0xFFFF
+
+
+def curves_from_rows(hist, M, row_w):
+    """Device weighted prefix scan of histogram rows -> int64 numerators
+    [n_desc, M+1] (or [batch, n_desc, M+1])."""
+    t = torch()
+    L = _lib.load()
+    dev = hist.device
+    batch = hist.shape[0] if hist.dim() == 3 else 1
+    n_rows = hist.shape[-2]
+    w = t.from_numpy(np.ascontiguousarray(np.asarray(row_w, np.int64))).to(dev)
+    n_desc = w.shape[0]
+    out = t.empty((n_desc, M + 1) if batch == 1 else (batch, n_desc, M + 1), dtype=t.int64, device=dev)
+    rc = L.ft_curves(ctypes.c_void_p(hist.data_ptr()), n_rows, M, batch, n_desc, ctypes.c_void_p(w.data_ptr()),
+                     ctypes.c_void_p(out.data_ptr()), _stream_ptr(dev))
+    _lib.check(rc, "ft_curves")
+    return out
+
+
 def class_weights(ndim, eighths):
     tables = TRANSITIONS_3D if ndim == 3 else TRANSITIONS_2D
     w = np.asarray(eighths, np.int64)

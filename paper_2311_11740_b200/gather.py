@@ -1,4 +1,4 @@
-"""Gather drivers: source -> device transition histogram.
+"""Gather drivers: source -> device histogram (map or fused-curve kind).
 
 Replaces the reference drivers gather_{2d,3d}_{serial,parallel} and their
 sliding-window streaming loops (contrib2d.py:235-294, contrib3d.py:392-458,
@@ -7,17 +7,24 @@ _parallel.py:8-33) with:
 * resident sources (``MemorySource``, ``DeviceSource``): one launch per vertex
   row block on the field already in HBM;
 * streamed sources (``ArraySource``, ``BmpSource``, ``RawVolumeSource``):
-  chunks of cell rows/planes read into two pinned host buffers and copied to
-  two device buffers on a side stream, so the read + H2D of chunk c+1 overlaps
-  the kernel on chunk c.  Chunk c covers vertex rows [a, b) and holds cell
-  rows [a-1, b-1]; the one-row halo is simply re-read (DESIGN.md §6);
+  chunks of cell rows/planes in pinned host memory are copied to two device
+  buffers on a side stream, so the H2D of chunk c+1 overlaps the kernel on
+  chunk c.  Chunk c covers vertex rows [a, b) and holds cell rows [a-1, b-1];
+  the one-row halo is simply re-sent.  A source that is
+  already a pinned torch tensor is copied straight from its own pages; any
+  other source is read into two pinned staging buffers first;
 * several GPUs in one process (``devices=[...]``): vertex-row slabs per GPU
   like split_blocks, histograms summed after the join.
 
-Every path produces the same histogram bit for bit: integer sums commute.
+``kind`` selects the kernel family: "map" = transition-class histograms
+(ft_hist2d/3d -> contribution maps), "lattice" = element histograms
+(ft_lattice2d/3d -> curves only).  Every path gives the same histogram bit
+for bit: integer sums commute.
 """
 
 from __future__ import annotations
+
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -27,23 +34,44 @@ from ._parallel import split_blocks
 DEFAULT_CHUNK_BYTES = 256 << 20
 
 
+@dataclass(frozen=True)
+class Kind:
+    name: str = "map"
+    maxes: bool = False
+
+    def new(self, ndim, M, device, batch=1):
+        if self.name == "map":
+            return engine.new_hist(ndim, M, device, batch)
+        return engine.new_lattice_hist(ndim, M, device, batch)
+
+    def launch(self, ndim, x, shape, M, quant, rows, first=0, hist=None, batch=1, batch_stride=0):
+        if self.name == "map":
+            return engine.launch_hist(ndim, x, shape, M, quant, rows=rows, first=first, hist=hist, batch=batch,
+                                      batch_stride=batch_stride)
+        return engine.launch_lattice(ndim, x, shape, M, quant, rows=rows, first=first, hist=hist, batch=batch,
+                                     batch_stride=batch_stride, maxes=self.maxes)
+
+
+MAP = Kind("map")
+
+
 def _torch_dtype(np_dtype):
     t = engine.torch()
     return {np.dtype(np.int32): t.int32, np.dtype(np.uint8): t.uint8, np.dtype(np.uint16): t.uint16,
             np.dtype(np.float32): t.float32}[np.dtype(np_dtype)]
 
 
-def resident_hist(src, ndim, device, rows, workers=1, hist=None):
+def resident_hist(src, ndim, device, rows, workers=1, hist=None, kind=MAP):
     x, quant = src.device_field(device)
     if hist is None:
-        hist = engine.new_hist(ndim, src.max_level, device)
+        hist = kind.new(ndim, src.max_level, device)
     v0, v1 = rows
     for a, b in split_blocks(v1 - v0, workers):
-        engine.launch_hist(ndim, x, src.shape, src.max_level, quant, rows=(v0 + a, v0 + b), hist=hist)
+        kind.launch(ndim, x, src.shape, src.max_level, quant, (v0 + a, v0 + b), hist=hist)
     return hist
 
 
-def stream_hist(src, ndim, device, rows, chunk_bytes=DEFAULT_CHUNK_BYTES, hist=None):
+def stream_hist(src, ndim, device, rows, chunk_bytes=DEFAULT_CHUNK_BYTES, hist=None, kind=MAP):
     """Double-buffered pinned-host -> HBM streaming of a source's rows/planes."""
     t = engine.torch()
     H = src.height
@@ -55,10 +83,12 @@ def stream_hist(src, ndim, device, rows, chunk_bytes=DEFAULT_CHUNK_BYTES, hist=N
     cap = min(cap, H + 1)
     vpc = max(1, cap - 1)  # vertex rows per chunk (one halo row)
     if hist is None:
-        hist = engine.new_hist(ndim, M, device)
-    pinned = [t.empty(cap * row_elems, dtype=tdt, pin_memory=True) for _ in range(2)]
+        hist = kind.new(ndim, M, device)
+    host = getattr(src, "pinned_rows", None)  # a pinned torch tensor (rows, ...) or None
+    if host is None:
+        staging = [t.empty(cap * row_elems, dtype=tdt, pin_memory=True) for _ in range(2)]
+        src.note_resident(2 * cap * row_elems * itemsize)
     dbuf = [t.empty(cap * row_elems, dtype=tdt, device=device) for _ in range(2)]
-    src.note_resident(2 * cap * row_elems * itemsize)
     compute = t.cuda.current_stream(device)
     copy = t.cuda.Stream(device)
     copied = [t.cuda.Event() for _ in range(2)]
@@ -69,33 +99,37 @@ def stream_hist(src, ndim, device, rows, chunk_bytes=DEFAULT_CHUNK_BYTES, hist=N
         s = c & 1
         r0, r1 = max(a - 1, 0), min(b - 1, H - 1) + 1
         n = (r1 - r0) * row_elems
-        if done[s] is not None:
-            done[s].synchronize()  # pinned[s] / dbuf[s] free again
-        src.read_rows(r0, r1, pinned[s].numpy()[:n])
+        if host is None:
+            if done[s] is not None:
+                done[s].synchronize()  # staging[s] free again
+            src.read_rows(r0, r1, staging[s].numpy()[:n])
+            chunk = staging[s][:n]
+        else:
+            chunk = host[r0 - src.pinned_first:r1 - src.pinned_first].reshape(-1)
         with t.cuda.stream(copy):
             if done[s] is not None:
-                copy.wait_event(done[s])
-            dbuf[s][:n].copy_(pinned[s][:n], non_blocking=True)
+                copy.wait_event(done[s])  # dbuf[s] consumed by the previous kernel
+            dbuf[s][:n].copy_(chunk, non_blocking=True)
             copied[s].record(copy)
         compute.wait_event(copied[s])
         view = dbuf[s][:n].view((r1 - r0,) + tuple(src.shape[1:]))
-        engine.launch_hist(ndim, view, src.shape, M, src.quant, rows=(a, b), first=r0, hist=hist)
+        kind.launch(ndim, view, src.shape, M, src.quant, (a, b), first=r0, hist=hist)
         ev = t.cuda.Event()
         ev.record(compute)
         done[s] = ev
     return hist
 
 
-def source_hist(src, ndim, device=None, workers=1, rows=None, chunk_bytes=DEFAULT_CHUNK_BYTES):
-    """Transition histogram of ``src`` for vertex rows ``rows`` on one GPU."""
+def source_hist(src, ndim, device=None, workers=1, rows=None, chunk_bytes=DEFAULT_CHUNK_BYTES, kind=MAP):
+    """Histogram of ``src`` for vertex rows ``rows`` on one GPU."""
     dev = engine.default_device(device)
     rows = rows if rows is not None else (0, src.height + 1)
     if src.mode in ("in-memory", "device"):
-        return resident_hist(src, ndim, dev, rows, workers)
-    return stream_hist(src, ndim, dev, rows, chunk_bytes)
+        return resident_hist(src, ndim, dev, rows, workers, kind=kind)
+    return stream_hist(src, ndim, dev, rows, chunk_bytes, kind=kind)
 
 
-def multi_device_hist(src, ndim, devices, chunk_bytes=DEFAULT_CHUNK_BYTES):
+def multi_device_hist(src, ndim, devices, chunk_bytes=DEFAULT_CHUNK_BYTES, kind=MAP):
     """Vertex-row slabs over several GPUs of this process; returns the summed
     histogram on devices[0].  Resident host fields upload only each slab's
     planes plus the one-plane halo."""
@@ -106,13 +140,13 @@ def multi_device_hist(src, ndim, devices, chunk_bytes=DEFAULT_CHUNK_BYTES):
         if src.mode == "in-memory":
             r0, r1 = max(a - 1, 0), min(b - 1, src.height - 1) + 1
             x = engine.to_device(src.field.values[r0:r1], dev)
-            h = engine.new_hist(ndim, src.max_level, dev)
-            parts.append(engine.launch_hist(ndim, x, src.shape, src.max_level,
-                                            engine.QuantSpec.identity(), rows=(a, b), first=r0, hist=h))
+            h = kind.new(ndim, src.max_level, dev)
+            parts.append(kind.launch(ndim, x, src.shape, src.max_level, engine.QuantSpec.identity(), (a, b),
+                                     first=r0, hist=h))
         elif src.mode == "device":
             raise ValueError("a DeviceSource lives on one GPU; use devices=None")
         else:
-            parts.append(stream_hist(src, ndim, dev, (a, b), chunk_bytes))
+            parts.append(stream_hist(src, ndim, dev, (a, b), chunk_bytes, kind=kind))
     total = parts[0]
     for p in parts[1:]:
         total += p.to(devs[0])

@@ -138,14 +138,15 @@ class QuantSpec:
         if h2 == l2:
             return QuantSpec(_lib.FT_Q_TABLE, int(negate), 0.0, 0.0, lo, hi, int(max_level))
         scale = np.float32(max_level / (h2 - l2))
-        bias = np.float32(0.5 - l2 * float(scale))
+        # estimate floor(x*scale + bias) = floor(y - 0.5) lands on L or L-1
+        bias = np.float32(-l2 * float(scale))
         # error of fmaf(x, scale, bias) against the float64 formula for x in
         # the window where the level is not clamped; beyond +-1 level the
         # kernel walks the table instead of a single correction step
         xmax = max(abs(l2), abs(h2)) + (h2 - l2)
         err = (xmax * abs(float(scale)) + abs(float(bias))) * 2.0 ** -22 + \
             abs(float(scale) * (h2 - l2) - max_level) + 1e-6
-        mode = _lib.FT_Q_TABLE if err < 0.45 else _lib.FT_Q_TABLE_ROBUST
+        mode = _lib.FT_Q_TABLE if err < 0.45 and not negate else _lib.FT_Q_TABLE_ROBUST
         return QuantSpec(mode, int(negate), float(scale), float(bias), lo, hi, int(max_level))
 
     @property
