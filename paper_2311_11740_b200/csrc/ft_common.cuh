@@ -80,8 +80,9 @@ __device__ __forceinline__ uint32_t to_level4(typename Elem<DT>::T raw, const fl
 {
     if constexpr (QM == FT_Q_TABLE) {
         const float x = (float)raw;
-        const int est = min(max(__float2int_rd(fmaf(x, scale, bias)), 0), M);
-        const uint32_t e4 = (uint32_t)est << 2;
+        // unsigned floor conversion saturates negatives (and NaN) to 0: one clamp
+        const uint32_t est = min(__float2uint_rd(fmaf(x, scale, bias)), (uint32_t)M);
+        const uint32_t e4 = est << 2;
         const float t = *reinterpret_cast<const float*>(reinterpret_cast<const char*>(tt) + e4 + 4);
         return x >= t ? e4 + 4 : e4;
     } else {

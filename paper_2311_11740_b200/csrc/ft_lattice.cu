@@ -3,30 +3,33 @@
 // The curve path of the north star: "evaluate each vertex's integer EC and
 // measure contributions into a filtration-level histogram, then a device
 // prefix scan".  Instead of classifying sorted neighbourhoods, count the
-// cells of the closed cubical complex by the level at which they appear:
-// an element (face, edge, vertex) of the complex appears at the MIN level of
-// its incident cells, so
-//   EC_26C = V - E + F - C,  surface area = 2 F - 6 C,  volume = C     (3D)
-//   EC_8C = V - E + C,  EC_4C = C - E_max + V_max,  perimeter = 2E - 4C,
+// cells of the closed cubical complex by the level at which they appear: an
+// element (face, edge, vertex) appears at the MIN level of its incident cells,
+// so
+//   EC_26C = V - E + F - C,  surface area = 2F - 6C,  volume = C      (3D)
+//   EC_8C = V - E + C,  EC_4C = -3C + E + V_max,  perimeter = 2E - 4C,
 //   area = C                                                           (2D)
-// with V/E/F/C counted by level (E_max/V_max: all incident cells active =
-// MAX filters).  These are the reference's vertex-contribution curves
-// (descriptors.py:169-178 over contrib2d/3d maps) rewritten; tests pin them
-// to the reference golden curves.  No tie-breaking enters: min/max are
-// order-free, so the curves are bit-exact without sorting.
+// with V/E/F/C counted by level (V_max: all incident cells active = MAX
+// filter).  These are the reference's vertex-contribution curves
+// (descriptors.py:169-178 over contrib2d/3d maps) rewritten (lattice.py holds
+// the algebra; tests pin it to the reference golden curves).  No tie-breaking
+// enters -- min/max are order-free -- so the curves are bit-exact without a
+// sort.
 //
-// Every lattice point p = (i, j, k) owns its low-corner vertex, the three
-// edges and three faces leaving it in + directions... equivalently the
-// elements whose incident cells are c - {0,1}^S (c = cell (i,j,k)).  Per
-// point: 3 face mins, 3 edge mins, 1 vertex min (7 VIMNMX on 16-bit pairs:
-// two lattice points per instruction) and 8 shared-memory increments into 4
-// histograms [cells, faces, edges, vertices].  Absent cells carry the
-// sentinel M+1 (elements touching only absent cells land in bin M+1, which
-// no curve reads), so tiles simply pad with sentinels: no boundary kernel.
+// Every lattice point p = (i, j, k) owns the elements whose incident cells
+// are c - {0,1}^S, c = cell (i, j, k): the cube, three faces, three edges and
+// the vertex.  Per point: 7 packed 16-bit mins (two points per VIMNMX) and 8
+// shared-memory increments into 4 histograms.  Absent cells carry the
+// sentinel M+1 (elements touching only absent cells land in bin M+1, which no
+// curve reads), so tiles pad with sentinels and need no boundary kernel.
 //
-// Layout: levels are staged as 16-bit (level * 4) in shared memory, two
-// k-adjacent cells per 32-bit word, so packed mins and the per-event
-// byte-address extraction are one instruction each.
+// Layout (3D): a 512-thread CTA stages a 16 x 32-word plane tile per step,
+// one word (two k-adjacent cells, levels * 4 as 16-bit lanes) per thread, and
+// 15 x 31 threads compute 15 lattice rows x 62 lattice columns from it (row
+// 0 / word 0 are the low halo).  One global load per thread per plane keeps
+// the warps balanced at the per-plane barrier.  Histogram rows sit 4 KB apart
+// (M <= 1022) so every event is one LOP/LEA + one ATOMS with an immediate
+// offset.
 #include <algorithm>
 
 #include "ft_common.cuh"
@@ -34,17 +37,16 @@
 
 namespace ft {
 
-constexpr int LTW = 32;                 // words (2 lattice points) per tile row = one warp
-constexpr int LTJ = 16;                 // tile rows (warps)
-constexpr int LNT = LTW * LTJ;          // 512 threads
-constexpr int LPW = LTW + 1;            // staged words per row (one halo word on the low side)
-constexpr int LPN = (LTJ + 1) * LPW;    // staged words per plane
-constexpr int LLD = (LPN + LNT - 1) / LNT;
-constexpr int LPF = 2;                  // planes in flight
+constexpr int LTW = 32;              // staged words per tile row (one warp)
+constexpr int LTJ = 16;              // staged rows (warps)
+constexpr int LNT = LTW * LTJ;       // 512 threads, one staged word each
+constexpr int LCW = LTW - 1;         // compute words per row (31 -> 62 lattice columns)
+constexpr int LCJ = LTJ - 1;         // compute rows (15)
+constexpr int HS_FIX = 4096;         // histogram row stride in bytes when M + 2 <= 1024
 
 struct LGeo {
     int64_t H, W, D, v0, v1, first, bstride;
-    int M, tiles_j, tiles_k, chunk;
+    int M, tiles_j, tiles_k, chunk, hs;
     int64_t n_items, items_per_image;
 };
 
@@ -53,11 +55,13 @@ __device__ __forceinline__ uint32_t vmax2(uint32_t a, uint32_t b) { return __vma
 // (hi half of a, lo half of b): the pair shifted down by one cell
 __device__ __forceinline__ uint32_t shift_pair(uint32_t a, uint32_t b) { return __byte_perm(a, b, 0x5432); }
 
-__device__ __forceinline__ void inc2(uint32_t* __restrict__ h, uint32_t w)
+// w holds two byte offsets (level * 4) of two lattice points
+template <int HS>
+__device__ __forceinline__ void inc2(char* __restrict__ h, int row, int hs, uint32_t w)
 {
-    // w holds two byte offsets (level * 4) of two lattice points
-    atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(h) + (w & 0xFFFFu)), 1u);
-    atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(h) + (w >> 16)), 1u);
+    const int off = HS ? row * HS : row * hs;
+    atomicAdd(reinterpret_cast<uint32_t*>(h + off + (w & 0xFFFFu)), 1u);
+    atomicAdd(reinterpret_cast<uint32_t*>(h + off + (w >> 16)), 1u);
 }
 
 template <int DT>
@@ -83,175 +87,177 @@ __device__ __forceinline__ typename Pair<DT>::T load_pair(const typename Elem<DT
     return v;
 }
 
+// Branch-free: quantize both cells unconditionally, then select the sentinel.
 template <int DT, int QM>
 __device__ __forceinline__ uint32_t pack_pair(const typename Pair<DT>::T& v, bool okx, bool oky, const float* tt,
                                               const QuantDev& q, int M, uint32_t sent4)
 {
-    const uint32_t a = okx ? to_level4<DT, QM>(v.x, tt, q.scale, q.bias, q.negate, M) : sent4;
-    const uint32_t b = oky ? to_level4<DT, QM>(v.y, tt, q.scale, q.bias, q.negate, M) : sent4;
+    uint32_t a = to_level4<DT, QM>(v.x, tt, q.scale, q.bias, q.negate, M);
+    uint32_t b = to_level4<DT, QM>(v.y, tt, q.scale, q.bias, q.negate, M);
+    a = okx ? a : sent4;
+    b = oky ? b : sent4;
     return __byte_perm(a, b, 0x5410);
+}
+
+__device__ __forceinline__ void flush_rows(uint32_t* h, unsigned long long* __restrict__ out, int nrows, int M2,
+                                           int hs_words, bool zero)
+{
+    for (int i = threadIdx.x; i < nrows * M2; i += blockDim.x) {
+        const int r = i / M2, l = i - r * M2;
+        uint32_t* p = h + r * hs_words + l;
+        const uint32_t v = *p;
+        if (v) atomicAdd(&out[i], (unsigned long long)v);
+        if (zero) *p = 0;
+    }
 }
 
 // ------------------------------------------------------------------- 3D
 
-template <int DT, int QM, bool VEC>
+template <int DT, int QM, bool VEC, int HS>
 __global__ void __launch_bounds__(LNT) lattice3d_kernel(const typename Elem<DT>::T* __restrict__ buf, LGeo g,
                                                          QuantDev q, unsigned long long* __restrict__ hist)
 {
     using P2 = typename Pair<DT>::T;
+    using T = typename Elem<DT>::T;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int M2 = g.M + 2;
-    uint32_t* h = reinterpret_cast<uint32_t*>(smem_raw);  // [4][M2]: cells, faces, edges, vertices
-    float* tt = reinterpret_cast<float*>(h + 4 * M2);
-    uint32_t* pl = reinterpret_cast<uint32_t*>(tt + M2);  // [2][LPN] words
-    for (int i = threadIdx.x; i < 4 * M2; i += LNT) h[i] = 0;
+    const int hs = HS ? HS : g.hs;                       // bytes between histogram rows
+    char* h = reinterpret_cast<char*>(smem_raw);          // rows: cells, faces, edges, vertices
+    float* tt = reinterpret_cast<float*>(h + 4 * hs);
+    uint32_t* pl = reinterpret_cast<uint32_t*>(tt + M2);  // [2][LNT] staged words
+    for (int i = threadIdx.x; i < hs; i += LNT) reinterpret_cast<uint32_t*>(h)[i] = 0;  // 4 rows = hs words
     if (QM != FT_Q_IDENTITY)
         for (int i = threadIdx.x; i < M2; i += LNT) tt[i] = q.tt[i];
     __syncthreads();
-    uint32_t* hv = h;
-    uint32_t* hf = h + M2;
-    uint32_t* he = h + 2 * M2;
-    uint32_t* hx = h + 3 * M2;
 
     const int tid = threadIdx.x;
     const int ty = tid / LTW, tx = tid % LTW;
+    const bool computes = ty < LCJ && tx < LCW;
     const int Wi = (int)g.W, Di = (int)g.D;
     const int64_t plane_elems = g.W * g.D;
-    const uint32_t sent2 = ((uint32_t)(g.M + 1) * 4u) * 0x10001u;
+    const uint32_t sent4 = (uint32_t)(g.M + 1) * 4u;
     const int64_t per_chunk = (int64_t)g.tiles_j * g.tiles_k;
     const int64_t it0 = g.n_items * blockIdx.x / gridDim.x;
     const int64_t it1 = g.n_items * (blockIdx.x + 1) / gridDim.x;
-
-    int lr[LLD], lw[LLD];
-#pragma unroll
-    for (int e = 0; e < LLD; ++e) {
-        const int idx = tid + e * LNT;
-        lr[e] = idx / LPW;
-        lw[e] = idx % LPW;
-    }
+    // this thread computes staged word (ty+1, tx+1): cur row word cw, row above cw-LTW
+    const int cw = (ty + 1) * LTW + tx + 1;
 
     for (int64_t item = it0; item < it1; ++item) {
         const int64_t ch = item / per_chunk;
         const int rem = (int)(item - ch * per_chunk);
-        const int j0 = (rem / g.tiles_k) * LTJ;
-        const int k0 = (rem % g.tiles_k) * (2 * LTW);
+        const int j0 = (rem / g.tiles_k) * LCJ;
+        const int k0 = (rem % g.tiles_k) * (2 * LCW);
         const int64_t ia = g.v0 + ch * g.chunk;
         const int64_t ib = min(ia + (int64_t)g.chunk, g.v1);
 
-        // staged word (r, w) = cells (row j0-1+r, cols k0-2+2w and +1)
-        int off[LLD];
-        bool okx[LLD], oky[LLD];
-#pragma unroll
-        for (int e = 0; e < LLD; ++e) {
-            const int jj = j0 - 1 + lr[e], kk = k0 - 2 + 2 * lw[e];
-            const bool row = (tid + e * LNT < LPN) && jj >= 0 && jj < Wi && kk >= 0;
-            okx[e] = row && kk < Di;
-            oky[e] = row && kk + 1 < Di;
-            off[e] = okx[e] ? jj * Di + kk : 0;
-        }
-        auto fetch = [&](int64_t p, P2 (&dst)[LLD]) {
-            const bool pin = p >= 0 && p < g.H;
-            const typename Elem<DT>::T* base = buf + (pin ? (p - g.first) * plane_elems : 0);
-#pragma unroll
-            for (int e = 0; e < LLD; ++e) dst[e] = load_pair<DT, VEC>(base + off[e], pin && okx[e], pin && oky[e]);
+        // staged word (ty, tx) = cells (row j0-1+ty, cols k0-2+2tx and +1)
+        const int jj = j0 - 1 + ty, kk = k0 - 2 + 2 * tx;
+        const bool row_ok = jj >= 0 && jj < Wi && kk >= 0;
+        const bool okx = row_ok && kk < Di, oky = row_ok && kk + 1 < Di;
+        // pointer to this word in plane ia-1 (bumped by one plane per step)
+        const T* ptr = buf + ((ia - 1 - g.first) * plane_elems + (okx ? (int64_t)jj * Di + kk : 0));
+        // planes are addressed relative to ia-1: t = 0 .. n+1; plane ia-1+t
+        // exists iff t_lo <= t < t_hi (32-bit, uniform)
+        const int n = (int)(ib - ia);
+        const int t_lo = ia >= 1 ? 0 : (int)(1 - ia);
+        const int t_hi = (int)min((int64_t)(n + 2), g.H - ia + 1);
+        auto fetch = [&](int t, const T* at) {
+            const bool pin = t >= t_lo && t < t_hi;
+            return load_pair<DT, VEC>(at, pin && okx, pin && oky);
         };
-        const uint32_t sent4 = (uint32_t)(g.M + 1) * 4u;
-        auto store = [&](int64_t p, uint32_t* dstp, const P2 (&src)[LLD]) {
-            const bool pin = p >= 0 && p < g.H;
-#pragma unroll
-            for (int e = 0; e < LLD; ++e) {
-                const int idx = tid + e * LNT;
-                if (idx < LPN) dstp[idx] = pack_pair<DT, QM>(src[e], pin && okx[e], pin && oky[e], tt, q, g.M, sent4);
-            }
+        auto store = [&](int t, uint32_t* dstp, const P2& v) {
+            const bool pin = t >= t_lo && t < t_hi;
+            dstp[tid] = pack_pair<DT, QM>(v, pin && okx, pin && oky, tt, q, g.M, sent4);
         };
-        // raw ring without register moves: ra holds the next even step's
-        // plane, rb the next odd step's; each is refilled right after use
-        P2 ra[LLD], rb[LLD];
-        fetch(ia - 1, ra);
-        store(ia - 1, pl, ra);
-        fetch(ia, ra);
-        fetch(ia + 1, rb);
+        // raw ring without register moves: ra feeds even steps, rb odd steps
+        P2 ra = fetch(0, ptr);
+        store(0, pl, ra);
+        ra = fetch(1, ptr + plane_elems);
+        P2 rb = fetch(2, ptr + 2 * plane_elems);
+        ptr += 3 * plane_elems;  // next fetch: t = 3
         __syncthreads();
 
-        // thread = lattice points (j0+ty, k0+2tx .. +1): cur row word cw
-        const int cw = (ty + 1) * LPW + tx + 1;
-        uint32_t W_ = pl[cw], U = pl[cw - LPW];
-        uint32_t Wm = shift_pair(pl[cw - 1], W_), Um = shift_pair(pl[cw - LPW - 1], U);
+        uint32_t W_ = pl[cw], U = pl[cw - LTW];
         uint32_t pW = W_;
-        uint32_t pm2k = vmin2(W_, Wm);
+        uint32_t pm2k = vmin2(W_, shift_pair(pl[cw - 1], W_));
         uint32_t pm2j = vmin2(W_, U);
-        uint32_t pm4i = vmin2(pm2k, vmin2(U, Um));
+        uint32_t pm4i = vmin2(pm2k, vmin2(U, shift_pair(pl[cw - LTW - 1], U)));
 
         auto step = [&](const uint32_t* cur) {
+            if (!computes) return;
             W_ = cur[cw];
-            U = cur[cw - LPW];
-            Wm = shift_pair(cur[cw - 1], W_);
-            Um = shift_pair(cur[cw - LPW - 1], U);
+            U = cur[cw - LTW];
+            const uint32_t Wm = shift_pair(cur[cw - 1], W_);
+            const uint32_t Um = shift_pair(cur[cw - LTW - 1], U);
             const uint32_t m2k = vmin2(W_, Wm);             // face normal k
             const uint32_t m2j = vmin2(W_, U);              // face normal j
             const uint32_t m4i = vmin2(m2k, vmin2(U, Um));  // edge along i
-            inc2(hv, W_);
-            inc2(hf, vmin2(W_, pW));     // face normal i
-            inc2(hf, m2j);
-            inc2(hf, m2k);
-            inc2(he, m4i);
-            inc2(he, vmin2(m2k, pm2k));  // edge along j
-            inc2(he, vmin2(m2j, pm2j));  // edge along k
-            inc2(hx, vmin2(m4i, pm4i));  // vertex
+            inc2<HS>(h, 0, hs, W_);
+            inc2<HS>(h, 1, hs, vmin2(W_, pW));     // face normal i
+            inc2<HS>(h, 1, hs, m2j);
+            inc2<HS>(h, 1, hs, m2k);
+            inc2<HS>(h, 2, hs, m4i);
+            inc2<HS>(h, 2, hs, vmin2(m2k, pm2k));  // edge along j
+            inc2<HS>(h, 2, hs, vmin2(m2j, pm2j));  // edge along k
+            inc2<HS>(h, 3, hs, vmin2(m4i, pm4i));  // vertex
             pW = W_;
             pm2k = m2k;
             pm2j = m2j;
             pm4i = m4i;
         };
-        for (int64_t i = ia; i < ib; i += 2) {
-            uint32_t* cur = pl + LPN;  // plane i (i - ia even) -> buffer 1
-            store(i, cur, ra);
-            if (i + 2 < ib) fetch(i + 2, ra);
+        for (int s = 0; s < n; s += 2) {
+            // step s: lattice row ia+s from plane t = s+1 (buffer 1)
+            uint32_t* cur = pl + LNT;
+            store(s + 1, cur, ra);
+            if (s + 2 < n) ra = fetch(s + 3, ptr);
+            ptr += plane_elems;
             __syncthreads();
             step(cur);
-            if (i + 1 >= ib) break;
-            cur = pl;                  // plane i + 1 -> buffer 0
-            store(i + 1, cur, rb);
-            if (i + 3 < ib) fetch(i + 3, rb);
+            if (s + 1 >= n) break;
+            cur = pl;  // step s+1: plane t = s+2 (buffer 0)
+            store(s + 2, cur, rb);
+            if (s + 3 < n) rb = fetch(s + 4, ptr);
+            ptr += plane_elems;
             __syncthreads();
             step(cur);
         }
         __syncthreads();
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < 4 * M2; i += LNT) {
-        const uint32_t v = h[i];
-        if (v) atomicAdd(&hist[i], (unsigned long long)v);
-    }
+    flush_rows(reinterpret_cast<uint32_t*>(h), hist, 4, M2, hs / 4, false);
 }
 
 // ------------------------------------------------------------------- 2D
-// Lattice point p = (i, j) owns its low-corner vertex (cells (i-1..i,
-// j-1..j)), the edge to (i, j+1) (cells (i-1, j), (i, j)), the edge to
-// (i+1, j) (cells (i, j-1), (i, j)) and the cell (i, j).  Rows: cells, edge
+// Lattice point p = (i, j) owns the cell (i, j), the edge to (i, j+1) (cells
+// (i-1, j), (i, j)), the edge to (i+1, j) (cells (i, j-1), (i, j)) and its
+// low-corner vertex (cells (i-1..i, j-1..j)).  Rows: cells, edge mins, vertex
 // mins, vertex maxes (the last only for EC_4C; E_max = 4C - E is implied).
-constexpr int L2W = 256;                 // words per row segment (512 lattice columns)
-constexpr int L2N = L2W + 1;
+// A 256-thread CTA stages one row segment of 256 words per step (one per
+// thread) and 255 threads compute 510 lattice columns.
+constexpr int L2W = 256;
+constexpr int L2C = L2W - 1;
 
-template <int DT, int QM, bool MAXES, bool VEC>
+template <int DT, int QM, bool MAXES, bool VEC, int HS>
 __global__ void __launch_bounds__(L2W) lattice2d_kernel(const typename Elem<DT>::T* __restrict__ buf, LGeo g,
                                                          QuantDev q, unsigned long long* __restrict__ hist)
 {
     using P2 = typename Pair<DT>::T;
+    using T = typename Elem<DT>::T;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int M2 = g.M + 2;
     constexpr int NR = 4;
-    uint32_t* h = reinterpret_cast<uint32_t*>(smem_raw);
-    float* tt = reinterpret_cast<float*>(h + NR * M2);
-    uint32_t* rows = reinterpret_cast<uint32_t*>(tt + M2);  // [2][L2N]
-    for (int i = threadIdx.x; i < NR * M2; i += L2W) h[i] = 0;
+    const int hs = HS ? HS : g.hs;
+    char* h = reinterpret_cast<char*>(smem_raw);
+    float* tt = reinterpret_cast<float*>(h + NR * hs);
+    uint32_t* rows = reinterpret_cast<uint32_t*>(tt + M2);  // [2][L2W]
+    for (int i = threadIdx.x; i < hs; i += L2W) reinterpret_cast<uint32_t*>(h)[i] = 0;
     if (QM != FT_Q_IDENTITY)
         for (int i = threadIdx.x; i < M2; i += L2W) tt[i] = q.tt[i];
     __syncthreads();
-    uint32_t *hc = h, *he = h + M2, *hx = h + 2 * M2, *hX = h + 3 * M2;
 
     const int tid = threadIdx.x;
-    const uint32_t sent2 = ((uint32_t)(g.M + 1) * 4u) * 0x10001u;
+    const bool computes = tid < L2C;
+    const uint32_t sent4 = (uint32_t)(g.M + 1) * 4u;
     const int Wi = (int)g.W;
     const int64_t it0 = g.n_items * blockIdx.x / gridDim.x;
     const int64_t it1 = g.n_items * (blockIdx.x + 1) / gridDim.x;
@@ -259,79 +265,73 @@ __global__ void __launch_bounds__(L2W) lattice2d_kernel(const typename Elem<DT>:
 
     for (int64_t item = it0; item < it1; ++item) {
         const int64_t b = item / g.items_per_image;
-        if (b != cur_img) {
+        if (b != cur_img) {  // histograms belong to one image: flush on change
             __syncthreads();
-            for (int i = threadIdx.x; i < NR * M2; i += L2W) {
-                const uint32_t v = h[i];
-                if (v) atomicAdd(&hist[cur_img * NR * M2 + i], (unsigned long long)v);
-                h[i] = 0;
-            }
+            flush_rows(reinterpret_cast<uint32_t*>(h), hist + cur_img * NR * M2, NR, M2, hs / 4, true);
             __syncthreads();
             cur_img = b;
         }
         const int64_t rem = item - b * g.items_per_image;
         const int64_t ch = rem / g.tiles_k;
-        const int j0 = (int)(rem % g.tiles_k) * (2 * L2W);
+        const int j0 = (int)(rem % g.tiles_k) * (2 * L2C);
         const int64_t ia = g.v0 + ch * g.chunk;
         const int64_t ib = min(ia + (int64_t)g.chunk, g.v1);
-        const typename Elem<DT>::T* img = buf + b * g.bstride;
-        // staged word w = cells (j0-2+2w, +1); thread tid owns word tid+1,
-        // thread 0 also loads word 0
-        const int kk0 = j0 - 2 + 2 * (tid + 1), kk1 = j0 - 2;
-        const bool ok0x = kk0 >= 0 && kk0 < Wi, ok0y = kk0 >= 0 && kk0 + 1 < Wi;
-        const bool ok1x = (tid == 0) && kk1 >= 0 && kk1 < Wi, ok1y = (tid == 0) && kk1 >= 0 && kk1 + 1 < Wi;
-        const uint32_t sent4 = (uint32_t)(g.M + 1) * 4u;
-        P2 raw[LPF + 1][2];
-        auto fetch = [&](int64_t r, P2 (&dst)[2]) {
-            const bool rin = r >= 0 && r < g.H;
-            const auto* base = img + (rin ? (r - g.first) * g.W : 0);
-            dst[0] = load_pair<DT, VEC>(base + (ok0x ? kk0 : 0), rin && ok0x, rin && ok0y);
-            dst[1] = load_pair<DT, VEC>(base + (ok1x ? kk1 : 0), rin && ok1x, rin && ok1y);
+        // staged word tid = cells (j0-2+2tid, +1); thread tid computes word tid+1
+        const int kk = j0 - 2 + 2 * tid;
+        const bool okx = kk >= 0 && kk < Wi, oky = kk >= 0 && kk + 1 < Wi;
+        const T* ptr = buf + b * g.bstride + ((ia - 1 - g.first) * g.W + (okx ? kk : 0));
+        // rows relative to ia-1: t = 0 .. n+1 (see the 3D kernel)
+        const int n = (int)(ib - ia);
+        const int t_lo = ia >= 1 ? 0 : (int)(1 - ia);
+        const int t_hi = (int)min((int64_t)(n + 2), g.H - ia + 1);
+        auto fetch = [&](int t, const T* at) {
+            const bool rin = t >= t_lo && t < t_hi;
+            return load_pair<DT, VEC>(at, rin && okx, rin && oky);
         };
-        auto store = [&](int64_t r, uint32_t* dst, const P2 (&src)[2]) {
-            const bool rin = r >= 0 && r < g.H;
-            dst[tid + 1] = pack_pair<DT, QM>(src[0], rin && ok0x, rin && ok0y, tt, q, g.M, sent4);
-            if (tid == 0) dst[0] = pack_pair<DT, QM>(src[1], rin && ok1x, rin && ok1y, tt, q, g.M, sent4);
+        auto store = [&](int t, uint32_t* dst, const P2& v) {
+            const bool rin = t >= t_lo && t < t_hi;
+            dst[tid] = pack_pair<DT, QM>(v, rin && okx, rin && oky, tt, q, g.M, sent4);
         };
-        fetch(ia - 1, raw[0]);
-#pragma unroll
-        for (int s = 1; s <= LPF; ++s) fetch(ia - 1 + s, raw[s]);
-        store(ia - 1, rows, raw[0]);
+        P2 ra = fetch(0, ptr);
+        store(0, rows, ra);
+        ra = fetch(1, ptr + g.W);
+        P2 rb = fetch(2, ptr + 2 * g.W);
+        ptr += 3 * g.W;
         __syncthreads();
         uint32_t pW = rows[tid + 1];
         uint32_t pWm = shift_pair(rows[tid], pW);
-        for (int64_t i = ia; i < ib; ++i) {
-            uint32_t* cur = rows + ((i - ia + 1) & 1) * L2N;
-            store(i, cur, raw[1]);
-#pragma unroll
-            for (int s = 1; s < LPF; ++s) {
-                raw[s][0] = raw[s + 1][0];
-                raw[s][1] = raw[s + 1][1];
-            }
-            if (i + LPF < ib) fetch(i + LPF, raw[LPF]);
-            __syncthreads();
+        auto step = [&](const uint32_t* cur) {
+            if (!computes) return;
             const uint32_t W_ = cur[tid + 1];
             const uint32_t Wm = shift_pair(cur[tid], W_);
-            const uint32_t eh = vmin2(W_, pW);            // edge (i,j)-(i,j+1): cells (i-1,j), (i,j)
-            const uint32_t ev = vmin2(W_, Wm);            // edge (i,j)-(i+1,j): cells (i,j-1), (i,j)
-            inc2(hc, W_);
-            inc2(he, eh);
-            inc2(he, ev);
-            inc2(hx, vmin2(ev, vmin2(pW, pWm)));
-            if constexpr (MAXES) {
-                inc2(hX, vmax2(vmax2(W_, Wm), vmax2(pW, pWm)));
-            }
+            const uint32_t ev = vmin2(W_, Wm);  // edge (i,j)-(i+1,j): cells (i,j-1), (i,j)
+            inc2<HS>(h, 0, hs, W_);
+            inc2<HS>(h, 1, hs, vmin2(W_, pW));  // edge (i,j)-(i,j+1): cells (i-1,j), (i,j)
+            inc2<HS>(h, 1, hs, ev);
+            inc2<HS>(h, 2, hs, vmin2(ev, vmin2(pW, pWm)));
+            if constexpr (MAXES) inc2<HS>(h, 3, hs, vmax2(vmax2(W_, Wm), vmax2(pW, pWm)));
             pW = W_;
             pWm = Wm;
+        };
+        for (int s = 0; s < n; s += 2) {
+            uint32_t* cur = rows + L2W;
+            store(s + 1, cur, ra);
+            if (s + 2 < n) ra = fetch(s + 3, ptr);
+            ptr += g.W;
+            __syncthreads();
+            step(cur);
+            if (s + 1 >= n) break;
+            cur = rows;
+            store(s + 2, cur, rb);
+            if (s + 3 < n) rb = fetch(s + 4, ptr);
+            ptr += g.W;
+            __syncthreads();
+            step(cur);
         }
         __syncthreads();
     }
     __syncthreads();
-    if (it0 < it1)
-        for (int i = threadIdx.x; i < NR * M2; i += L2W) {
-            const uint32_t v = h[i];
-            if (v) atomicAdd(&hist[cur_img * NR * M2 + i], (unsigned long long)v);
-        }
+    if (it0 < it1) flush_rows(reinterpret_cast<uint32_t*>(h), hist + cur_img * NR * M2, NR, M2, hs / 4, false);
 }
 
 static int nsm_l()
@@ -347,31 +347,45 @@ static QuantDev qdev(const ft_quant* qa)
                     qa ? qa->thresholds : nullptr};
 }
 
+// histogram row stride in bytes: the fixed 4 KB (immediate offsets) when it fits
+static int row_stride(int M) { return (M + 2) * 4 <= HS_FIX ? HS_FIX : ((M + 2) * 4 + 15) / 16 * 16; }
+
+// Work split: tiles x row-chunks, contiguous item ranges per CTA, enough
+// items (>= ~6 per CTA) to balance while keeping marches long.
+static void plan_items(LGeo& g, int64_t tiles, int64_t batch, int64_t grid_cap, int64_t min_rows)
+{
+    const int64_t rows = g.v1 - g.v0;
+    int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>(cdiv(6 * grid_cap, tiles * batch), rows / min_rows));
+    g.chunk = (int)cdiv(rows, nchunks);
+    nchunks = cdiv(rows, g.chunk);
+    g.items_per_image = tiles * nchunks;
+    g.n_items = g.items_per_image * batch;
+}
+
 template <int DT, int QM>
 static int launch_l3(const ft_window* win, int64_t H, int64_t W, int64_t D, int64_t v0, int64_t v1,
                      const ft_quant* qa, int32_t M, uint64_t* hist, cudaStream_t st)
 {
+    using T = typename Elem<DT>::T;
     LGeo g{};
     g.H = H; g.W = W; g.D = D; g.v0 = v0; g.v1 = v1; g.first = win->first; g.M = M;
-    const size_t smem = (size_t)(5 * (M + 2)) * 4 + 2 * LPN * 4;
-    auto kern = (D % 2 == 0 && reinterpret_cast<uintptr_t>(win->data) % 8 == 0) ? lattice3d_kernel<DT, QM, true>
-                                                                                 : lattice3d_kernel<DT, QM, false>;
+    g.hs = row_stride(M);
+    const size_t smem = (size_t)4 * g.hs + (size_t)(M + 2) * 4 + 2 * LNT * 4;
+    const bool vec = D % 2 == 0 && reinterpret_cast<uintptr_t>(win->data) % 8 == 0;
+    const bool fix = g.hs == HS_FIX;
+    auto kern = vec ? (fix ? lattice3d_kernel<DT, QM, true, HS_FIX> : lattice3d_kernel<DT, QM, true, 0>)
+                    : (fix ? lattice3d_kernel<DT, QM, false, HS_FIX> : lattice3d_kernel<DT, QM, false, 0>);
     FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     FT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, LNT, smem));
     if (per_sm < 1) return FT_ERR_ARG;
     // lattice points j in [0, W], k in [0, D] (the high boundary included)
-    g.tiles_j = (int)cdiv(W + 1, LTJ);
-    g.tiles_k = (int)cdiv(D + 1, 2 * LTW);
-    const int64_t tiles = (int64_t)g.tiles_j * g.tiles_k;
-    const int64_t rows = v1 - v0;
+    g.tiles_j = (int)cdiv(W + 1, LCJ);
+    g.tiles_k = (int)cdiv(D + 1, 2 * LCW);
     const int64_t grid_cap = (int64_t)nsm_l() * per_sm;
-    int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>(cdiv(6 * grid_cap, tiles), rows / 32));
-    g.chunk = (int)cdiv(rows, nchunks);
-    nchunks = cdiv(rows, g.chunk);
-    g.n_items = tiles * nchunks;
+    plan_items(g, (int64_t)g.tiles_j * g.tiles_k, 1, grid_cap, 32);
     const int grid = (int)std::min<int64_t>(grid_cap, g.n_items);
-    kern<<<grid, LNT, smem, st>>>(static_cast<const typename Elem<DT>::T*>(win->data), g, qdev(qa),
+    kern<<<grid, LNT, smem, st>>>(static_cast<const T*>(win->data), g, qdev(qa),
                                   reinterpret_cast<unsigned long long*>(hist));
     FT_CUDA_TRY(cudaGetLastError());
     return FT_OK;
@@ -381,30 +395,34 @@ template <int DT, int QM>
 static int launch_l2(const ft_window* win, int64_t H, int64_t W, int64_t v0, int64_t v1, const ft_quant* qa,
                      int32_t M, int maxes, uint64_t* hist, cudaStream_t st)
 {
+    using T = typename Elem<DT>::T;
     LGeo g{};
     g.H = H; g.W = W; g.D = 1; g.v0 = v0; g.v1 = v1; g.first = win->first; g.M = M;
     g.bstride = win->batch_stride;
+    g.hs = row_stride(M);
     const int64_t batch = std::max<int64_t>(win->batch, 1);
-    const size_t smem = (size_t)(5 * (M + 2)) * 4 + 2 * L2N * 4;
-    const bool vec = W % 2 == 0 && (win->batch <= 1 || win->batch_stride % 2 == 0) &&
+    const size_t smem = (size_t)4 * g.hs + (size_t)(M + 2) * 4 + 2 * L2W * 4;
+    const bool vec = W % 2 == 0 && (batch <= 1 || win->batch_stride % 2 == 0) &&
                      reinterpret_cast<uintptr_t>(win->data) % 8 == 0;
-    auto kern = maxes ? (vec ? lattice2d_kernel<DT, QM, true, true> : lattice2d_kernel<DT, QM, true, false>)
-                      : (vec ? lattice2d_kernel<DT, QM, false, true> : lattice2d_kernel<DT, QM, false, false>);
+    const bool fix = g.hs == HS_FIX;
+    using K = void (*)(const T*, LGeo, QuantDev, unsigned long long*);
+    K kern;
+    if (maxes) {
+        if (vec) kern = fix ? lattice2d_kernel<DT, QM, true, true, HS_FIX> : lattice2d_kernel<DT, QM, true, true, 0>;
+        else kern = fix ? lattice2d_kernel<DT, QM, true, false, HS_FIX> : lattice2d_kernel<DT, QM, true, false, 0>;
+    } else {
+        if (vec) kern = fix ? lattice2d_kernel<DT, QM, false, true, HS_FIX> : lattice2d_kernel<DT, QM, false, true, 0>;
+        else kern = fix ? lattice2d_kernel<DT, QM, false, false, HS_FIX> : lattice2d_kernel<DT, QM, false, false, 0>;
+    }
     FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     FT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L2W, smem));
     if (per_sm < 1) return FT_ERR_ARG;
-    g.tiles_k = (int)cdiv(W + 1, 2 * L2W);
-    const int64_t rows = v1 - v0;
+    g.tiles_k = (int)cdiv(W + 1, 2 * L2C);
     const int64_t grid_cap = (int64_t)nsm_l() * per_sm;
-    const int64_t tiles_all = (int64_t)g.tiles_k * batch;
-    int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>(cdiv(4 * grid_cap, tiles_all), rows / 64));
-    g.chunk = (int)cdiv(rows, nchunks);
-    nchunks = cdiv(rows, g.chunk);
-    g.items_per_image = g.tiles_k * nchunks;
-    g.n_items = g.items_per_image * batch;
+    plan_items(g, g.tiles_k, batch, grid_cap, 64);
     const int grid = (int)std::min<int64_t>(grid_cap, g.n_items);
-    kern<<<grid, L2W, smem, st>>>(static_cast<const typename Elem<DT>::T*>(win->data), g, qdev(qa),
+    kern<<<grid, L2W, smem, st>>>(static_cast<const T*>(win->data), g, qdev(qa),
                                   reinterpret_cast<unsigned long long*>(hist));
     FT_CUDA_TRY(cudaGetLastError());
     return FT_OK;
