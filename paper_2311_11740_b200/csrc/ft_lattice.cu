@@ -27,10 +27,12 @@
 // one word (two k-adjacent cells, levels * 4 as 16-bit lanes) per thread, and
 // 15 x 31 threads compute 15 lattice rows x 62 lattice columns from it (row
 // 0 / word 0 are the low halo).  One global load per thread per plane keeps
-// the warps balanced at the per-plane barrier.  Histogram rows sit 4 KB apart
-// (M <= 1022) so every event is one LOP/LEA + one ATOMS with an immediate
-// offset.
+// the warps balanced at the per-plane barrier.  Each event is one LOP/LEA
+// (extract a 16-bit byte offset) + one ATOMS on a uniform row base; the
+// histograms are privatised per lane group to keep those ATOMS bank-conflict
+// free (see Priv below).
 #include <algorithm>
+#include <cstdlib>
 
 #include "ft_common.cuh"
 #include "ft_tables.h"
@@ -42,7 +44,7 @@ constexpr int LTJ = 16;              // staged rows (warps)
 constexpr int LNT = LTW * LTJ;       // 512 threads, one staged word each
 constexpr int LCW = LTW - 1;         // compute words per row (31 -> 62 lattice columns)
 constexpr int LCJ = LTJ - 1;         // compute rows (15)
-constexpr int HS_FIX = 4096;         // histogram row stride in bytes when M + 2 <= 1024
+
 
 struct LGeo {
     int64_t H, W, D, v0, v1, first, bstride;
@@ -55,14 +57,24 @@ __device__ __forceinline__ uint32_t vmax2(uint32_t a, uint32_t b) { return __vma
 // (hi half of a, lo half of b): the pair shifted down by one cell
 __device__ __forceinline__ uint32_t shift_pair(uint32_t a, uint32_t b) { return __byte_perm(a, b, 0x5432); }
 
-// w holds two byte offsets (level * 4) of two lattice points
-template <int HS>
+// w holds two byte offsets (level * 4 * CP + copy * 4) of two lattice points;
+// row bases are uniform, so each event is one extract + one ATOMS
 __device__ __forceinline__ void inc2(char* __restrict__ h, int row, int hs, uint32_t w)
 {
-    const int off = HS ? row * HS : row * hs;
-    atomicAdd(reinterpret_cast<uint32_t*>(h + off + (w & 0xFFFFu)), 1u);
-    atomicAdd(reinterpret_cast<uint32_t*>(h + off + (w >> 16)), 1u);
+    char* base = h + row * hs;
+    atomicAdd(reinterpret_cast<uint32_t*>(base + (w & 0xFFFFu)), 1u);
+    atomicAdd(reinterpret_cast<uint32_t*>(base + (w >> 16)), 1u);
 }
+
+// Histograms are privatised CP ways by lane: bin (level, copy) sits at
+// (level * CP + copy) words, copy = lane % CP, so two lanes can only meet in
+// a bank if they share lane % CP -- the bank-conflict degree of the event
+// ATOMS drops from ~2.2 wavefronts to ~1 (profiles/r01).  The copy offset is
+// added to the loaded level words once per step (mins commute with it).
+template <int CP>
+struct Priv {
+    static constexpr int SH = CP == 8 ? 3 : CP == 4 ? 2 : CP == 2 ? 1 : 0;
+};
 
 template <int DT>
 struct Pair;
@@ -88,40 +100,48 @@ __device__ __forceinline__ typename Pair<DT>::T load_pair(const typename Elem<DT
 }
 
 // Branch-free: quantize both cells unconditionally, then select the sentinel.
-template <int DT, int QM>
+// Output lanes hold level * 4 << SH (byte offsets of copy 0).
+template <int DT, int QM, int SH>
 __device__ __forceinline__ uint32_t pack_pair(const typename Pair<DT>::T& v, bool okx, bool oky, const float* tt,
-                                              const QuantDev& q, int M, uint32_t sent4)
+                                              const QuantDev& q, int M, uint32_t sent)
 {
-    uint32_t a = to_level4<DT, QM>(v.x, tt, q.scale, q.bias, q.negate, M);
-    uint32_t b = to_level4<DT, QM>(v.y, tt, q.scale, q.bias, q.negate, M);
-    a = okx ? a : sent4;
-    b = oky ? b : sent4;
+    uint32_t a = to_level4<DT, QM>(v.x, tt, q.scale, q.bias, q.negate, M) << SH;
+    uint32_t b = to_level4<DT, QM>(v.y, tt, q.scale, q.bias, q.negate, M) << SH;
+    a = okx ? a : sent;
+    b = oky ? b : sent;
     return __byte_perm(a, b, 0x5410);
 }
 
+// Sum the CP copies of every (row, level) bin into the global histogram.
+template <int CP>
 __device__ __forceinline__ void flush_rows(uint32_t* h, unsigned long long* __restrict__ out, int nrows, int M2,
                                            int hs_words, bool zero)
 {
     for (int i = threadIdx.x; i < nrows * M2; i += blockDim.x) {
         const int r = i / M2, l = i - r * M2;
-        uint32_t* p = h + r * hs_words + l;
-        const uint32_t v = *p;
+        uint32_t* p = h + r * hs_words + l * CP;
+        uint32_t v = 0;
+#pragma unroll
+        for (int c = 0; c < CP; ++c) {
+            v += p[c];
+            if (zero) p[c] = 0;
+        }
         if (v) atomicAdd(&out[i], (unsigned long long)v);
-        if (zero) *p = 0;
     }
 }
 
 // ------------------------------------------------------------------- 3D
 
-template <int DT, int QM, bool VEC, int HS>
+template <int DT, int QM, bool VEC, int CP>
 __global__ void __launch_bounds__(LNT) lattice3d_kernel(const typename Elem<DT>::T* __restrict__ buf, LGeo g,
                                                          QuantDev q, unsigned long long* __restrict__ hist)
 {
     using P2 = typename Pair<DT>::T;
     using T = typename Elem<DT>::T;
+    constexpr int SH = Priv<CP>::SH;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int M2 = g.M + 2;
-    const int hs = HS ? HS : g.hs;                       // bytes between histogram rows
+    const int hs = g.hs;                                  // bytes between histogram rows
     char* h = reinterpret_cast<char*>(smem_raw);          // rows: cells, faces, edges, vertices
     float* tt = reinterpret_cast<float*>(h + 4 * hs);
     uint32_t* pl = reinterpret_cast<uint32_t*>(tt + M2);  // [2][LNT] staged words
@@ -135,7 +155,8 @@ __global__ void __launch_bounds__(LNT) lattice3d_kernel(const typename Elem<DT>:
     const bool computes = ty < LCJ && tx < LCW;
     const int Wi = (int)g.W, Di = (int)g.D;
     const int64_t plane_elems = g.W * g.D;
-    const uint32_t sent4 = (uint32_t)(g.M + 1) * 4u;
+    const uint32_t sent4 = ((uint32_t)(g.M + 1) * 4u) << SH;
+    const uint32_t cpy = (uint32_t)(tid % CP) * 4u * 0x10001u;  // this lane's histogram copy, both halves
     const int64_t per_chunk = (int64_t)g.tiles_j * g.tiles_k;
     const int64_t it0 = g.n_items * blockIdx.x / gridDim.x;
     const int64_t it1 = g.n_items * (blockIdx.x + 1) / gridDim.x;
@@ -167,7 +188,7 @@ __global__ void __launch_bounds__(LNT) lattice3d_kernel(const typename Elem<DT>:
         };
         auto store = [&](int t, uint32_t* dstp, const P2& v) {
             const bool pin = t >= t_lo && t < t_hi;
-            dstp[tid] = pack_pair<DT, QM>(v, pin && okx, pin && oky, tt, q, g.M, sent4);
+            dstp[tid] = pack_pair<DT, QM, SH>(v, pin && okx, pin && oky, tt, q, g.M, sent4);
         };
         // raw ring without register moves: ra feeds even steps, rb odd steps
         P2 ra = fetch(0, ptr);
@@ -177,29 +198,30 @@ __global__ void __launch_bounds__(LNT) lattice3d_kernel(const typename Elem<DT>:
         ptr += 3 * plane_elems;  // next fetch: t = 3
         __syncthreads();
 
-        uint32_t W_ = pl[cw], U = pl[cw - LTW];
+        // loaded words carry this lane's copy offset (no carry: lanes < 2^16)
+        uint32_t W_ = pl[cw] + cpy, U = pl[cw - LTW] + cpy;
         uint32_t pW = W_;
-        uint32_t pm2k = vmin2(W_, shift_pair(pl[cw - 1], W_));
+        uint32_t pm2k = vmin2(W_, shift_pair(pl[cw - 1] + cpy, W_));
         uint32_t pm2j = vmin2(W_, U);
-        uint32_t pm4i = vmin2(pm2k, vmin2(U, shift_pair(pl[cw - LTW - 1], U)));
+        uint32_t pm4i = vmin2(pm2k, vmin2(U, shift_pair(pl[cw - LTW - 1] + cpy, U)));
 
         auto step = [&](const uint32_t* cur) {
             if (!computes) return;
-            W_ = cur[cw];
-            U = cur[cw - LTW];
-            const uint32_t Wm = shift_pair(cur[cw - 1], W_);
-            const uint32_t Um = shift_pair(cur[cw - LTW - 1], U);
+            W_ = cur[cw] + cpy;
+            U = cur[cw - LTW] + cpy;
+            const uint32_t Wm = shift_pair(cur[cw - 1] + cpy, W_);
+            const uint32_t Um = shift_pair(cur[cw - LTW - 1] + cpy, U);
             const uint32_t m2k = vmin2(W_, Wm);             // face normal k
             const uint32_t m2j = vmin2(W_, U);              // face normal j
             const uint32_t m4i = vmin2(m2k, vmin2(U, Um));  // edge along i
-            inc2<HS>(h, 0, hs, W_);
-            inc2<HS>(h, 1, hs, vmin2(W_, pW));     // face normal i
-            inc2<HS>(h, 1, hs, m2j);
-            inc2<HS>(h, 1, hs, m2k);
-            inc2<HS>(h, 2, hs, m4i);
-            inc2<HS>(h, 2, hs, vmin2(m2k, pm2k));  // edge along j
-            inc2<HS>(h, 2, hs, vmin2(m2j, pm2j));  // edge along k
-            inc2<HS>(h, 3, hs, vmin2(m4i, pm4i));  // vertex
+            inc2(h, 0, hs, W_);
+            inc2(h, 1, hs, vmin2(W_, pW));     // face normal i
+            inc2(h, 1, hs, m2j);
+            inc2(h, 1, hs, m2k);
+            inc2(h, 2, hs, m4i);
+            inc2(h, 2, hs, vmin2(m2k, pm2k));  // edge along j
+            inc2(h, 2, hs, vmin2(m2j, pm2j));  // edge along k
+            inc2(h, 3, hs, vmin2(m4i, pm4i));  // vertex
             pW = W_;
             pm2k = m2k;
             pm2j = m2j;
@@ -224,7 +246,7 @@ __global__ void __launch_bounds__(LNT) lattice3d_kernel(const typename Elem<DT>:
         __syncthreads();
     }
     __syncthreads();
-    flush_rows(reinterpret_cast<uint32_t*>(h), hist, 4, M2, hs / 4, false);
+    flush_rows<CP>(reinterpret_cast<uint32_t*>(h), hist, 4, M2, hs / 4, false);
 }
 
 // ------------------------------------------------------------------- 2D
@@ -237,16 +259,17 @@ __global__ void __launch_bounds__(LNT) lattice3d_kernel(const typename Elem<DT>:
 constexpr int L2W = 256;
 constexpr int L2C = L2W - 1;
 
-template <int DT, int QM, bool MAXES, bool VEC, int HS>
+template <int DT, int QM, bool MAXES, bool VEC, int CP>
 __global__ void __launch_bounds__(L2W) lattice2d_kernel(const typename Elem<DT>::T* __restrict__ buf, LGeo g,
                                                          QuantDev q, unsigned long long* __restrict__ hist)
 {
     using P2 = typename Pair<DT>::T;
     using T = typename Elem<DT>::T;
+    constexpr int SH = Priv<CP>::SH;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int M2 = g.M + 2;
     constexpr int NR = 4;
-    const int hs = HS ? HS : g.hs;
+    const int hs = g.hs;
     char* h = reinterpret_cast<char*>(smem_raw);
     float* tt = reinterpret_cast<float*>(h + NR * hs);
     uint32_t* rows = reinterpret_cast<uint32_t*>(tt + M2);  // [2][L2W]
@@ -257,7 +280,8 @@ __global__ void __launch_bounds__(L2W) lattice2d_kernel(const typename Elem<DT>:
 
     const int tid = threadIdx.x;
     const bool computes = tid < L2C;
-    const uint32_t sent4 = (uint32_t)(g.M + 1) * 4u;
+    const uint32_t sent4 = ((uint32_t)(g.M + 1) * 4u) << SH;
+    const uint32_t cpy = (uint32_t)(tid % CP) * 4u * 0x10001u;
     const int Wi = (int)g.W;
     const int64_t it0 = g.n_items * blockIdx.x / gridDim.x;
     const int64_t it1 = g.n_items * (blockIdx.x + 1) / gridDim.x;
@@ -267,7 +291,7 @@ __global__ void __launch_bounds__(L2W) lattice2d_kernel(const typename Elem<DT>:
         const int64_t b = item / g.items_per_image;
         if (b != cur_img) {  // histograms belong to one image: flush on change
             __syncthreads();
-            flush_rows(reinterpret_cast<uint32_t*>(h), hist + cur_img * NR * M2, NR, M2, hs / 4, true);
+            flush_rows<CP>(reinterpret_cast<uint32_t*>(h), hist + cur_img * NR * M2, NR, M2, hs / 4, true);
             __syncthreads();
             cur_img = b;
         }
@@ -290,7 +314,7 @@ __global__ void __launch_bounds__(L2W) lattice2d_kernel(const typename Elem<DT>:
         };
         auto store = [&](int t, uint32_t* dst, const P2& v) {
             const bool rin = t >= t_lo && t < t_hi;
-            dst[tid] = pack_pair<DT, QM>(v, rin && okx, rin && oky, tt, q, g.M, sent4);
+            dst[tid] = pack_pair<DT, QM, SH>(v, rin && okx, rin && oky, tt, q, g.M, sent4);
         };
         P2 ra = fetch(0, ptr);
         store(0, rows, ra);
@@ -298,18 +322,18 @@ __global__ void __launch_bounds__(L2W) lattice2d_kernel(const typename Elem<DT>:
         P2 rb = fetch(2, ptr + 2 * g.W);
         ptr += 3 * g.W;
         __syncthreads();
-        uint32_t pW = rows[tid + 1];
-        uint32_t pWm = shift_pair(rows[tid], pW);
+        uint32_t pW = rows[tid + 1] + cpy;
+        uint32_t pWm = shift_pair(rows[tid] + cpy, pW);
         auto step = [&](const uint32_t* cur) {
             if (!computes) return;
-            const uint32_t W_ = cur[tid + 1];
-            const uint32_t Wm = shift_pair(cur[tid], W_);
+            const uint32_t W_ = cur[tid + 1] + cpy;
+            const uint32_t Wm = shift_pair(cur[tid] + cpy, W_);
             const uint32_t ev = vmin2(W_, Wm);  // edge (i,j)-(i+1,j): cells (i,j-1), (i,j)
-            inc2<HS>(h, 0, hs, W_);
-            inc2<HS>(h, 1, hs, vmin2(W_, pW));  // edge (i,j)-(i,j+1): cells (i-1,j), (i,j)
-            inc2<HS>(h, 1, hs, ev);
-            inc2<HS>(h, 2, hs, vmin2(ev, vmin2(pW, pWm)));
-            if constexpr (MAXES) inc2<HS>(h, 3, hs, vmax2(vmax2(W_, Wm), vmax2(pW, pWm)));
+            inc2(h, 0, hs, W_);
+            inc2(h, 1, hs, vmin2(W_, pW));  // edge (i,j)-(i,j+1): cells (i-1,j), (i,j)
+            inc2(h, 1, hs, ev);
+            inc2(h, 2, hs, vmin2(ev, vmin2(pW, pWm)));
+            if constexpr (MAXES) inc2(h, 3, hs, vmax2(vmax2(W_, Wm), vmax2(pW, pWm)));
             pW = W_;
             pWm = Wm;
         };
@@ -331,7 +355,7 @@ __global__ void __launch_bounds__(L2W) lattice2d_kernel(const typename Elem<DT>:
         __syncthreads();
     }
     __syncthreads();
-    if (it0 < it1) flush_rows(reinterpret_cast<uint32_t*>(h), hist + cur_img * NR * M2, NR, M2, hs / 4, false);
+    if (it0 < it1) flush_rows<CP>(reinterpret_cast<uint32_t*>(h), hist + cur_img * NR * M2, NR, M2, hs / 4, false);
 }
 
 static int nsm_l()
@@ -347,8 +371,30 @@ static QuantDev qdev(const ft_quant* qa)
                     qa ? qa->thresholds : nullptr};
 }
 
-// histogram row stride in bytes: the fixed 4 KB (immediate offsets) when it fits
-static int row_stride(int M) { return (M + 2) * 4 <= HS_FIX ? HS_FIX : ((M + 2) * 4 + 15) / 16 * 16; }
+// Privatisation degree: as many copies (8, 4 or 1) as keep the 16-bit packed
+// byte offsets in range and the 4 histogram rows within ~72 KB, so three
+// 512-thread CTAs still fit an SM.
+static int copies_for(int M)
+{
+    // Measured (profiles/r01/lattice_notes.md): with smooth fields the event
+    // levels of a warp are near-random mod 32, so splitting lanes into copy
+    // groups does not lower the conflict degree (2.5 wavefronts either way)
+    // while the larger footprint costs occupancy: 283 -> 257 Gvox/s at
+    // 2048^3.  Single copy unless FT_LATTICE_COPIES asks otherwise.
+    static const int forced = [] {
+        const char* e = getenv("FT_LATTICE_COPIES");
+        return e ? atoi(e) : 1;
+    }();
+    if (forced <= 1) return 1;
+    for (int cp : {8, 4, 2}) {
+        if (cp > forced) continue;
+        const int64_t bytes = (int64_t)(M + 2) * 4 * cp;
+        if ((int64_t)(M + 1) * 4 * cp + 4 * (cp - 1) <= 0xFFFF && 4 * bytes <= 72 * 1024) return cp;
+    }
+    return 1;
+}
+// histogram row stride in bytes for cp copies (16-byte aligned rows)
+static int row_stride(int M, int cp) { return ((M + 2) * 4 * cp + 15) / 16 * 16; }
 
 // Work split: tiles x row-chunks, contiguous item ranges per CTA, enough
 // items (>= ~6 per CTA) to balance while keeping marches long.
@@ -369,12 +415,16 @@ static int launch_l3(const ft_window* win, int64_t H, int64_t W, int64_t D, int6
     using T = typename Elem<DT>::T;
     LGeo g{};
     g.H = H; g.W = W; g.D = D; g.v0 = v0; g.v1 = v1; g.first = win->first; g.M = M;
-    g.hs = row_stride(M);
+    const int cp = copies_for(M);
+    g.hs = row_stride(M, cp);
     const size_t smem = (size_t)4 * g.hs + (size_t)(M + 2) * 4 + 2 * LNT * 4;
     const bool vec = D % 2 == 0 && reinterpret_cast<uintptr_t>(win->data) % 8 == 0;
-    const bool fix = g.hs == HS_FIX;
-    auto kern = vec ? (fix ? lattice3d_kernel<DT, QM, true, HS_FIX> : lattice3d_kernel<DT, QM, true, 0>)
-                    : (fix ? lattice3d_kernel<DT, QM, false, HS_FIX> : lattice3d_kernel<DT, QM, false, 0>);
+    using K = void (*)(const T*, LGeo, QuantDev, unsigned long long*);
+    K kern;
+    if (vec) kern = cp == 8 ? lattice3d_kernel<DT, QM, true, 8> : cp == 4 ? lattice3d_kernel<DT, QM, true, 4>
+                  : cp == 2 ? lattice3d_kernel<DT, QM, true, 2> : lattice3d_kernel<DT, QM, true, 1>;
+    else kern = cp == 8 ? lattice3d_kernel<DT, QM, false, 8> : cp == 4 ? lattice3d_kernel<DT, QM, false, 4>
+              : cp == 2 ? lattice3d_kernel<DT, QM, false, 2> : lattice3d_kernel<DT, QM, false, 1>;
     FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     FT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, LNT, smem));
@@ -399,20 +449,21 @@ static int launch_l2(const ft_window* win, int64_t H, int64_t W, int64_t v0, int
     LGeo g{};
     g.H = H; g.W = W; g.D = 1; g.v0 = v0; g.v1 = v1; g.first = win->first; g.M = M;
     g.bstride = win->batch_stride;
-    g.hs = row_stride(M);
+    // 2D: 8 copies only while they are small (many 256-thread CTAs per SM)
+    const int cp = (int64_t)(M + 2) * 4 * 8 * 4 <= 40 * 1024 ? 8 : 1;
+    g.hs = row_stride(M, cp);
     const int64_t batch = std::max<int64_t>(win->batch, 1);
     const size_t smem = (size_t)4 * g.hs + (size_t)(M + 2) * 4 + 2 * L2W * 4;
     const bool vec = W % 2 == 0 && (batch <= 1 || win->batch_stride % 2 == 0) &&
                      reinterpret_cast<uintptr_t>(win->data) % 8 == 0;
-    const bool fix = g.hs == HS_FIX;
     using K = void (*)(const T*, LGeo, QuantDev, unsigned long long*);
     K kern;
     if (maxes) {
-        if (vec) kern = fix ? lattice2d_kernel<DT, QM, true, true, HS_FIX> : lattice2d_kernel<DT, QM, true, true, 0>;
-        else kern = fix ? lattice2d_kernel<DT, QM, true, false, HS_FIX> : lattice2d_kernel<DT, QM, true, false, 0>;
+        if (vec) kern = cp == 8 ? lattice2d_kernel<DT, QM, true, true, 8> : lattice2d_kernel<DT, QM, true, true, 1>;
+        else kern = cp == 8 ? lattice2d_kernel<DT, QM, true, false, 8> : lattice2d_kernel<DT, QM, true, false, 1>;
     } else {
-        if (vec) kern = fix ? lattice2d_kernel<DT, QM, false, true, HS_FIX> : lattice2d_kernel<DT, QM, false, true, 0>;
-        else kern = fix ? lattice2d_kernel<DT, QM, false, false, HS_FIX> : lattice2d_kernel<DT, QM, false, false, 0>;
+        if (vec) kern = cp == 8 ? lattice2d_kernel<DT, QM, false, true, 8> : lattice2d_kernel<DT, QM, false, true, 1>;
+        else kern = cp == 8 ? lattice2d_kernel<DT, QM, false, false, 8> : lattice2d_kernel<DT, QM, false, false, 1>;
     }
     FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
