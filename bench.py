@@ -167,7 +167,7 @@ def main():
 
     import paper_2311_11740_b200 as ft
     from paper_2311_11740_b200 import engine, synth
-    from paper_2311_11740_b200._parallel import split_blocks
+    from paper_2311_11740_b200._parallel import held_rows, split_blocks
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -176,7 +176,7 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     blocks = split_blocks(H + 1, ws)
     a, b = blocks[rank] if rank < len(blocks) else (H + 1, H + 1)
-    r0, r1 = max(a - 1, 0), min(b - 1, H - 1) + 1
+    r0, r1 = held_rows(a, b, H)
 
     # ---- field (setup, untimed) -------------------------------------------
     x = synth.grf_slab(shape, sigma, args.seed, (r0, r1), dev)

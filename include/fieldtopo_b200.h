@@ -42,6 +42,8 @@ extern "C" {
 #define FT_Q_IDENTITY 0     /* the element IS the level */
 #define FT_Q_TABLE 1        /* quantize_with_range via threshold table (fast) */
 #define FT_Q_TABLE_ROBUST 2 /* same, for ill-conditioned ranges */
+#define FT_Q_POW2 3         /* lo == 0, hi == 2^p: exact without a table (scale = M/hi);
+                               kernels without a specialised path treat it as FT_Q_TABLE */
 
 #define FT_NCLASS_2D 6  /* transition classes, 2D */
 #define FT_NCLASS_3D 40 /* transition classes, 3D */
@@ -102,9 +104,10 @@ int ft_hist3d(const ft_window *win, int64_t H, int64_t W, int64_t D, int64_t v0,
  * (descriptors.py:83-97, 169-178) is an integer combination of the rows
  * (DESIGN.md §3b).  Lattice points cover [v0, v1) x [0, W] (x [0, D]).
  * 3D hist: device uint64 [4][M+2] rows (cells, face mins, edge mins,
- *   vertex mins); requires D even, (M+1)*4 <= 65535.
+ *   vertex mins); requires (M+1)*4 <= 65535 and, unlike ft_hist3d, the
+ *   window must also hold plane v0-2 (when >= 0).
  * 2D hist: device uint64 [batch][4][M+2] rows (cells, edge mins, vertex
- *   mins, vertex maxes; the last only when maxes != 0); requires W even.
+ *   mins, vertex maxes; the last only when maxes != 0).
  * Both accumulate, like ft_hist2d/3d. */
 int ft_lattice3d(const ft_window *win, int64_t H, int64_t W, int64_t D, int64_t v0, int64_t v1,
                  const ft_quant *q, int32_t M, uint64_t *hist, void *stream);

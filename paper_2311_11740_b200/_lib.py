@@ -13,7 +13,7 @@ from . import build as _build
 from ._tables import ClassificationError
 
 FT_I32, FT_U8, FT_U16, FT_F32, FT_F64 = 0, 1, 2, 3, 4
-FT_Q_IDENTITY, FT_Q_TABLE, FT_Q_TABLE_ROBUST = 0, 1, 2
+FT_Q_IDENTITY, FT_Q_TABLE, FT_Q_TABLE_ROBUST, FT_Q_POW2 = 0, 1, 2, 3
 FT_ERR_ARG, FT_ERR_CLASSIFY, FT_ERR_CUDA_BASE = 1, 2, 1000
 
 EXPORTS = ("ft_hist2d", "ft_hist3d", "ft_lattice2d", "ft_lattice3d", "ft_finalize", "ft_curves", "ft_class_weights", "ft_tables",

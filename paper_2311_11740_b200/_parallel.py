@@ -9,6 +9,18 @@ per-GPU slabs (``gather.multi_device_hist``) and per-rank slabs
 
 from __future__ import annotations
 
+# Cell rows/planes below its first vertex row a slab must hold: vertex row a
+# reads planes a-1 and a; the fused-curve kernel also signs the cells of
+# plane a-1, whose -i neighbour is plane a-2.
+LOW_HALO = 2
+
+
+def held_rows(v0, v1, H):
+    """Cell rows/planes [r0, r1) a slab of vertex rows [v0, v1) holds."""
+    r0 = max(v0 - LOW_HALO, 0)
+    r1 = max(min(v1 - 1, H - 1) + 1, r0)
+    return r0, r1
+
 
 def split_blocks(total, workers):
     if workers < 1:

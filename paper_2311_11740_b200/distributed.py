@@ -6,7 +6,8 @@ contrib2d.py:274-294, contrib3d.py:440-458).  Across GPUs the same contract
 becomes:
 
 * rank r owns vertex rows [v0, v1) = split_blocks(H + 1, world)[r] and holds
-  cell planes [v0 - 1, v1 - 1] (its own planes plus one halo plane);
+  cell planes [v0 - 2, v1 - 1] (its own planes plus the low halo planes:
+  one for the vertex neighbourhoods, one for the per-cell signatures);
 * each rank fills its histogram with the same kernels as a single GPU;
 * one ``all_reduce(SUM)`` of the small histogram (NCCL over NVLink on GPUs,
   gloo on CPU) -- the only exchange step -- after which every rank holds the
@@ -20,7 +21,7 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 from . import engine, gather
-from ._parallel import split_blocks
+from ._parallel import held_rows, split_blocks
 
 
 @dataclass(frozen=True)
@@ -51,8 +52,8 @@ def slab_for(H, world, rank):
     if rank >= len(blocks):  # more ranks than vertex rows
         return Slab(rank, world, H + 1, H + 1, H, H)
     v0, v1 = blocks[rank]
-    r0, r1 = max(v0 - 1, 0), min(v1 - 1, H - 1) + 1
-    return Slab(rank, world, v0, v1, r0, max(r1, r0))
+    r0, r1 = held_rows(v0, v1, H)
+    return Slab(rank, world, v0, v1, r0, r1)
 
 
 def all_reduce_hist(hist, group=None):

@@ -9,8 +9,8 @@ _parallel.py:8-33) with:
 * streamed sources (``ArraySource``, ``BmpSource``, ``RawVolumeSource``):
   chunks of cell rows/planes in pinned host memory are copied to two device
   buffers on a side stream, so the H2D of chunk c+1 overlaps the kernel on
-  chunk c.  Chunk c covers vertex rows [a, b) and holds cell rows [a-1, b-1];
-  the one-row halo is simply re-sent.  A source that is
+  chunk c.  Chunk c covers vertex rows [a, b) and holds cell rows
+  [a-2, b-1]; the low halo rows are simply re-sent.  A source that is
   already a pinned torch tensor is copied straight from its own pages; any
   other source is read into two pinned staging buffers first;
 * several GPUs in one process (``devices=[...]``): vertex-row slabs per GPU
@@ -29,7 +29,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import engine
-from ._parallel import split_blocks
+from ._parallel import LOW_HALO, held_rows, split_blocks
 
 DEFAULT_CHUNK_BYTES = 256 << 20
 
@@ -79,9 +79,9 @@ def stream_hist(src, ndim, device, rows, chunk_bytes=DEFAULT_CHUNK_BYTES, hist=N
     row_elems = src.width * (src.depth if ndim == 3 else 1)
     itemsize = np.dtype(src.dtype).itemsize
     tdt = _torch_dtype(src.dtype)
-    cap = max(2, int(chunk_bytes // max(1, row_elems * itemsize)))  # cell rows per buffer
+    cap = max(LOW_HALO + 1, int(chunk_bytes // max(1, row_elems * itemsize)))  # cell rows per buffer
     cap = min(cap, H + 1)
-    vpc = max(1, cap - 1)  # vertex rows per chunk (one halo row)
+    vpc = max(1, cap - LOW_HALO)  # vertex rows per chunk (LOW_HALO halo rows re-sent)
     if hist is None:
         hist = kind.new(ndim, M, device)
     host = getattr(src, "pinned_rows", None)  # a pinned torch tensor (rows, ...) or None
@@ -97,7 +97,7 @@ def stream_hist(src, ndim, device, rows, chunk_bytes=DEFAULT_CHUNK_BYTES, hist=N
     for c, a in enumerate(range(v0, v1, vpc)):
         b = min(a + vpc, v1)
         s = c & 1
-        r0, r1 = max(a - 1, 0), min(b - 1, H - 1) + 1
+        r0, r1 = held_rows(a, b, H)
         n = (r1 - r0) * row_elems
         if host is None:
             if done[s] is not None:
@@ -138,7 +138,7 @@ def multi_device_hist(src, ndim, devices, chunk_bytes=DEFAULT_CHUNK_BYTES, kind=
     parts = []
     for dev, (a, b) in zip(devs, blocks):
         if src.mode == "in-memory":
-            r0, r1 = max(a - 1, 0), min(b - 1, src.height - 1) + 1
+            r0, r1 = held_rows(a, b, src.height)
             x = engine.to_device(src.field.values[r0:r1], dev)
             h = kind.new(ndim, src.max_level, dev)
             parts.append(kind.launch(ndim, x, src.shape, src.max_level, engine.QuantSpec.identity(), (a, b),

@@ -147,6 +147,12 @@ class QuantSpec:
         err = (xmax * abs(float(scale)) + abs(float(bias))) * 2.0 ** -22 + \
             abs(float(scale) * (h2 - l2) - max_level) + 1e-6
         mode = _lib.FT_Q_TABLE if err < 0.45 and not negate else _lib.FT_Q_TABLE_ROBUST
+        if not negate and l2 == 0.0 and h2 > 0 and math.frexp(h2)[0] == 0.5 and max_level < (1 << 22):
+            # lo = 0, hi = 2^p: scale = M / hi is exact and the reference's
+            # float64 formula is exact for float32 inputs -> table-free mode
+            # (the table still ships for kernels that use it)
+            mode = _lib.FT_Q_POW2
+            scale, bias = np.float32(max_level / h2), np.float32(0.0)
         return QuantSpec(mode, int(negate), float(scale), float(bias), lo, hi, int(max_level))
 
     @property

@@ -22,8 +22,8 @@ def test_slab_plan_covers_every_vertex_row():
             rows = [v for s in slabs for v in range(s.v0, s.v1)]
             assert rows == list(range(H + 1))
             for s in slabs:
-                if not s.empty:  # planes needed by vertex rows [v0, v1)
-                    assert s.r0 == max(s.v0 - 1, 0) and s.r1 == min(s.v1 - 1, H - 1) + 1
+                if not s.empty:  # planes needed by vertex rows [v0, v1) (+ the signature halo)
+                    assert s.r0 == max(s.v0 - 2, 0) and s.r1 == min(s.v1 - 1, H - 1) + 1
     assert [(s.v0, s.v1) for s in (slab_for(10, 3, r) for r in range(3))] == split_blocks(11, 3)
     with pytest.raises(ValueError):
         slab_for(10, 0, 0)
