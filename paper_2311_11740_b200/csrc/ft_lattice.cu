@@ -33,6 +33,7 @@
 // free (see Priv below).
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "ft_common.cuh"
 #include "ft_tables.h"
@@ -427,6 +428,176 @@ __global__ void __launch_bounds__(SNT, 4) lattice3d_sig_kernel(const typename El
     }
 }
 
+// --------------------------------- 3D, register-blocked and barrier-free
+// The same booking as lattice3d_sig_kernel (5 shared atomics per lattice
+// point) without staging: every WARP independently owns a strip of R lattice
+// rows x 60 lattice columns and marches the planes.  Lane l holds the words
+// (two k-adjacent cells) of column pair l for the R+2 cell rows j0-1 .. j0+R
+// of the current plane in registers, so j-neighbours are registers and
+// k-neighbours one shuffle away; lanes 0 and 31 carry the halo columns.
+// Each lane loads and quantizes its own words (one 8-byte load per row per
+// plane, two planes in flight), so there is no shared staging, no LDS/STS and
+// no CTA barrier: the shared memory serves only the histograms.
+template <int DT, int QM, bool VEC, int R>
+__global__ void __launch_bounds__(256) lattice3d_rb_kernel(const typename Elem<DT>::T* __restrict__ buf, LGeo g,
+                                                           QuantDev q, unsigned long long* __restrict__ hist)
+{
+    using P2 = typename Pair<DT>::T;
+    using T = typename Elem<DT>::T;
+    constexpr int NR = R + 2;                              // cell rows held per plane
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int M2 = g.M + 2;
+    const int hs = g.hs;
+    char* h = reinterpret_cast<char*>(smem_raw);           // rows: sig u = 0..6, edges, vertices
+    float* tt = reinterpret_cast<float*>(h + 9 * hs);
+    for (int i = threadIdx.x; i < 9 * hs / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(h)[i] = 0;
+    if (QM != FT_Q_IDENTITY && QM != FT_Q_POW2)
+        for (int i = threadIdx.x; i < M2; i += blockDim.x) tt[i] = q.tt[i];
+    __syncthreads();
+    char* hsig = h;
+    char* hE = h + 7 * hs;
+    char* hV = h + 8 * hs;
+
+    const int lane = threadIdx.x & 31;
+    const bool computes = lane >= 1 && lane <= 30;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x / 32);
+    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int Wi = (int)g.W, Di = (int)g.D;
+    const int64_t plane_elems = g.W * g.D;
+    const uint32_t sent4 = (uint32_t)(g.M + 1) * 4u;
+    const uint32_t hs_pk = (uint32_t)hs;
+    const int64_t per_chunk = (int64_t)g.tiles_j * g.tiles_k;
+    const int64_t it0 = g.n_items * gw / nwarps;
+    const int64_t it1 = g.n_items * (gw + 1) / nwarps;
+
+    for (int64_t item = it0; item < it1; ++item) {
+        const int64_t ch = item / per_chunk;
+        const int rem = (int)(item - ch * per_chunk);
+        const int j0 = (rem / g.tiles_k) * R;
+        const int k0 = (rem % g.tiles_k) * 60;
+        const int64_t ia = g.v0 + ch * g.chunk;
+        const int64_t ib = min(ia + (int64_t)g.chunk, g.v1);
+        const int kk = k0 - 2 + 2 * lane;
+        const bool okx = kk >= 0 && kk < Di, oky = kk >= 0 && kk + 1 < Di;
+        uint32_t rowok = 0;  // bit r: cell row j0-1+r exists (warp-uniform)
+#pragma unroll
+        for (int r = 0; r < NR; ++r) rowok |= (j0 - 1 + r >= 0 && j0 - 1 + r < Wi) ? 1u << r : 0u;
+        const int n = (int)(ib - ia);
+        const int t_lo = (int)max((int64_t)-1, 1 - ia);
+        const int t_hi = (int)min((int64_t)(n + 2), g.H - ia + 1);
+        // word of row 0 in plane ia-2 (t = -1); rows are D elements apart
+        const T* ptr = buf + ((ia - 2 - g.first) * plane_elems + (int64_t)(j0 - 1) * Di + (okx ? kk : 0));
+        auto fetch = [&](int t, const T* at, P2 (&dst)[NR]) {
+            const bool pin = t >= t_lo && t < t_hi;
+#pragma unroll
+            for (int r = 0; r < NR; ++r) {
+                const bool ok = pin && ((rowok >> r) & 1u);
+                dst[r] = load_pair<DT, VEC>(at + r * Di, ok && okx, ok && oky);
+            }
+        };
+        auto quant = [&](int t, const P2 (&src)[NR], uint32_t (&V)[NR]) {
+            const bool pin = t >= t_lo && t < t_hi;
+#pragma unroll
+            for (int r = 0; r < NR; ++r) {
+                const bool ok = pin && ((rowok >> r) & 1u);
+                V[r] = pack_pair<DT, QM, 0>(src[r], ok && okx, ok && oky, tt, q, g.M, sent4);
+            }
+        };
+
+        uint32_t V[NR], pV[NR], ppV[NR], pWm[NR], pWp[NR], pm2k[NR], pm2j[NR], pm4i[NR];
+        P2 ra[NR], rb[NR];
+        // prologue: planes ia-2 (t = -1) and ia-1 (t = 0)
+        fetch(-1, ptr, ra);
+        fetch(0, ptr + plane_elems, rb);
+        quant(-1, ra, ppV);
+        quant(0, rb, pV);
+        fetch(1, ptr + 2 * plane_elems, ra);
+        fetch(2, ptr + 3 * plane_elems, rb);
+        ptr += 4 * plane_elems;  // next fetch: t = 3
+        {
+            uint32_t Wm[NR];
+#pragma unroll
+            for (int r = 0; r < NR; ++r) Wm[r] = shift_pair(__shfl_up_sync(0xFFFFFFFFu, pV[r], 1), pV[r]);
+#pragma unroll
+            for (int r = 1; r <= R; ++r) {
+                pWm[r] = Wm[r];
+                pWp[r] = shift_pair(pV[r], __shfl_down_sync(0xFFFFFFFFu, pV[r], 1));
+                pm2k[r] = vmin2(pV[r], Wm[r]);
+                pm2j[r] = vmin2(pV[r], pV[r - 1]);
+                pm4i[r] = vmin2(pm2k[r], vmin2(pV[r - 1], Wm[r - 1]));
+            }
+        }
+
+        auto step = [&]() {
+            uint32_t Wm[NR];
+#pragma unroll
+            for (int r = 0; r < NR; ++r) Wm[r] = shift_pair(__shfl_up_sync(0xFFFFFFFFu, V[r], 1), V[r]);
+#pragma unroll
+            for (int r = 1; r <= R; ++r) {
+                const uint32_t W_ = V[r], U = V[r - 1];
+                const uint32_t Wp = shift_pair(W_, __shfl_down_sync(0xFFFFFFFFu, W_, 1));
+                const uint32_t m2k = vmin2(W_, Wm[r]);             // face normal k
+                const uint32_t m2j = vmin2(W_, U);                 // face normal j
+                const uint32_t m4i = vmin2(m2k, vmin2(U, Wm[r - 1]));  // edge along i
+                if (computes) {
+                    inc2(hE, 0, hs, m4i);
+                    inc2(hE, 0, hs, vmin2(m2k, pm2k[r]));  // edge along j
+                    inc2(hE, 0, hs, vmin2(m2j, pm2j[r]));  // edge along k
+                    inc2(hV, 0, hs, vmin2(m4i, pm4i[r]));  // vertex
+                    // signature of the plane-(i-1) cells of row r (see lattice3d_sig_kernel)
+                    const uint32_t cb = pV[r] | 0x80008000u;
+                    const uint32_t r0 = cb - ppV[r];            // -i
+                    const uint32_t r1 = cb - pV[r - 1];         // -j
+                    const uint32_t r2 = cb - pWm[r];            // -k
+                    const uint32_t r3 = cb - W_ - 0x10001u;     // +i
+                    const uint32_t r4 = cb - pV[r + 1] - 0x10001u;  // +j
+                    const uint32_t r5 = cb - pWp[r] - 0x10001u;     // +k
+                    const uint32_t u = ((r0 >> 15) & 0x10001u) + ((r1 >> 15) & 0x10001u) +
+                                       ((r2 >> 15) & 0x10001u) + ((r3 >> 15) & 0x10001u) +
+                                       ((r4 >> 15) & 0x10001u) + ((r5 >> 15) & 0x10001u);
+                    inc2(hsig, 0, hs, u * hs_pk + pV[r]);
+                }
+                ppV[r] = pV[r];
+                pWm[r] = Wm[r];
+                pWp[r] = Wp;
+                pm2k[r] = m2k;
+                pm2j[r] = m2j;
+                pm4i[r] = m4i;
+            }
+#pragma unroll
+            for (int r = 0; r < NR; ++r) pV[r] = V[r];
+        };
+        for (int s = 0; s < n; s += 2) {
+            quant(s + 1, ra, V);  // plane t = s+1
+            if (s + 2 < n) fetch(s + 3, ptr, ra);
+            ptr += plane_elems;
+            step();
+            if (s + 1 >= n) break;
+            quant(s + 2, rb, V);
+            if (s + 3 < n) fetch(s + 4, ptr, rb);
+            ptr += plane_elems;
+            step();
+        }
+    }
+    __syncthreads();
+    const uint32_t* hw = reinterpret_cast<const uint32_t*>(h);
+    const int rw = hs / 4;
+    for (int l = threadIdx.x; l < M2; l += blockDim.x) {
+        uint32_t c = 0, f = 0;
+#pragma unroll
+        for (int u = 0; u < 7; ++u) {
+            const uint32_t v = hw[u * rw + l];
+            c += v;
+            f += (6 - u) * v;
+        }
+        const uint32_t e = hw[7 * rw + l], x = hw[8 * rw + l];
+        if (c) atomicAdd(&hist[l], (unsigned long long)c);
+        if (f) atomicAdd(&hist[M2 + l], (unsigned long long)f);
+        if (e) atomicAdd(&hist[2 * M2 + l], (unsigned long long)e);
+        if (x) atomicAdd(&hist[3 * M2 + l], (unsigned long long)x);
+    }
+}
+
 // ------------------------------------------------------------------- 2D
 // Lattice point p = (i, j) owns the cell (i, j), the edge to (i, j+1) (cells
 // (i-1, j), (i, j)), the edge to (i+1, j) (cells (i, j-1), (i, j)) and its
@@ -594,13 +765,33 @@ static int launch_l3(const ft_window* win, int64_t H, int64_t W, int64_t D, int6
     LGeo g{};
     g.H = H; g.W = W; g.D = D; g.v0 = v0; g.v1 = v1; g.first = win->first; g.M = M;
     const bool vec3 = D % 2 == 0 && reinterpret_cast<uintptr_t>(win->data) % 8 == 0;
+    static const char* which = getenv("FT_LATTICE_KERNEL");  // rb (default) | sig | staged
+    if ((!which || !strcmp(which, "rb")) && 6 * (((M + 2) * 4 + 15) / 16 * 16) + (M + 1) * 4 < 0xFFFF) {
+        constexpr int R = 4, NTH = 256;
+        g.hs = ((M + 2) * 4 + 15) / 16 * 16;
+        const size_t smem = (size_t)9 * g.hs + (size_t)(M + 2) * 4;
+        auto kern = vec3 ? lattice3d_rb_kernel<DT, QM, true, R> : lattice3d_rb_kernel<DT, QM, false, R>;
+        FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0;
+        FT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NTH, smem));
+        if (per_sm < 1) return FT_ERR_ARG;
+        g.tiles_j = (int)cdiv(W + 1, R);
+        g.tiles_k = (int)cdiv(D + 1, 60);
+        const int64_t grid_cap = (int64_t)nsm_l() * per_sm;
+        plan_items(g, (int64_t)g.tiles_j * g.tiles_k, 1, grid_cap * (NTH / 32), 32);
+        const int grid = (int)std::min<int64_t>(grid_cap, cdiv(g.n_items, NTH / 32));
+        kern<<<grid, NTH, smem, st>>>(static_cast<const T*>(win->data), g, qdev(qa),
+                                      reinterpret_cast<unsigned long long*>(hist));
+        FT_CUDA_TRY(cudaGetLastError());
+        return FT_OK;
+    }
     {
         // per-cell signature kernel when its packed row offsets fit 16 bits
         const int hs = ((M + 2) * 4 + 15) / 16 * 16;
         // Measured at 2048^3 (profiles/r01/lattice_notes.md): 298 Gvox/s vs
         // 308 for the 8-event kernel -- fewer ATOMS but more ALU and latency;
         // opt-in until the barrier-free variant lands.
-        static const bool sig = getenv("FT_LATTICE_SIG") != nullptr;
+        static const bool sig = which && !strcmp(which, "sig");
         if (sig && 6 * hs + (M + 1) * 4 < 0xFFFF) {
             g.hs = hs;
             const size_t smem = (size_t)9 * hs + (size_t)(M + 2) * 4 + 2 * SNT * 4;
