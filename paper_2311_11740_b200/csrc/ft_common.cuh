@@ -76,18 +76,17 @@ __device__ __forceinline__ uint32_t to_level(typename Elem<DT>::T raw, const flo
 // level * 4 (a shared-memory byte offset), for the 16-bit packed kernels.
 // FT_Q_POW2 (lo = 0, hi = 2^p, scale = M / hi exact): the reference's float64
 // (x - 0) * M / hi + 0.5 is exact for every float32 x (<= 47 significant
-// bits), so level = clamp(floor(x * scale + 0.5)).  fmaf rounds once, so its
-// floor is L or L + 1, and the sign of fmaf(x, scale, 0.5 - est) -- the exact
-// residual, rounded once -- says which: no table, no shared-memory load.
+// bits), so level = clamp(floor(x * scale + 0.5)).  The FMA rounded toward
+// -infinity never crosses an integer upward and every integer below 2^24 is a
+// float, so floor(fma_rd(x, scale, 0.5)) IS that floor: three instructions,
+// no table, no shared-memory load.
 template <int DT, int QM>
 __device__ __forceinline__ uint32_t to_level4(typename Elem<DT>::T raw, const float* __restrict__ tt, float scale,
                                               float bias, int negate, int M)
 {
     if constexpr (QM == FT_Q_POW2) {
         const float x = (float)raw;
-        uint32_t est = __float2uint_rd(fmaf(x, scale, 0.5f));  // saturates < 0 and NaN to 0
-        const float r = fmaf(x, scale, 0.5f - (float)est);
-        est -= (r < 0.f && est > 0u) ? 1u : 0u;
+        const uint32_t est = __float2uint_rd(__fmaf_rd(x, scale, 0.5f));  // saturates < 0 and NaN to 0
         return min(est, (uint32_t)M) << 2;
     } else if constexpr (QM == FT_Q_TABLE) {
         const float x = (float)raw;

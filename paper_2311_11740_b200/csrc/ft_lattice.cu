@@ -529,7 +529,7 @@ __global__ void __launch_bounds__(256) lattice3d_rb_kernel(const typename Elem<D
         }
 
         auto step = [&]() {
-            uint32_t Wm[NR];
+            uint32_t Wm[NR], ev[R + 1][5];
 #pragma unroll
             for (int r = 0; r < NR; ++r) Wm[r] = shift_pair(__shfl_up_sync(0xFFFFFFFFu, V[r], 1), V[r]);
 #pragma unroll
@@ -539,24 +539,21 @@ __global__ void __launch_bounds__(256) lattice3d_rb_kernel(const typename Elem<D
                 const uint32_t m2k = vmin2(W_, Wm[r]);             // face normal k
                 const uint32_t m2j = vmin2(W_, U);                 // face normal j
                 const uint32_t m4i = vmin2(m2k, vmin2(U, Wm[r - 1]));  // edge along i
-                if (computes) {
-                    inc2(hE, 0, hs, m4i);
-                    inc2(hE, 0, hs, vmin2(m2k, pm2k[r]));  // edge along j
-                    inc2(hE, 0, hs, vmin2(m2j, pm2j[r]));  // edge along k
-                    inc2(hV, 0, hs, vmin2(m4i, pm4i[r]));  // vertex
-                    // signature of the plane-(i-1) cells of row r (see lattice3d_sig_kernel)
-                    const uint32_t cb = pV[r] | 0x80008000u;
-                    const uint32_t r0 = cb - ppV[r];            // -i
-                    const uint32_t r1 = cb - pV[r - 1];         // -j
-                    const uint32_t r2 = cb - pWm[r];            // -k
-                    const uint32_t r3 = cb - W_ - 0x10001u;     // +i
-                    const uint32_t r4 = cb - pV[r + 1] - 0x10001u;  // +j
-                    const uint32_t r5 = cb - pWp[r] - 0x10001u;     // +k
-                    const uint32_t u = ((r0 >> 15) & 0x10001u) + ((r1 >> 15) & 0x10001u) +
-                                       ((r2 >> 15) & 0x10001u) + ((r3 >> 15) & 0x10001u) +
-                                       ((r4 >> 15) & 0x10001u) + ((r5 >> 15) & 0x10001u);
-                    inc2(hsig, 0, hs, u * hs_pk + pV[r]);
-                }
+                ev[r][0] = m4i;
+                ev[r][1] = vmin2(m2k, pm2k[r]);  // edge along j
+                ev[r][2] = vmin2(m2j, pm2j[r]);  // edge along k
+                ev[r][3] = vmin2(m4i, pm4i[r]);  // vertex
+                // signature of the plane-(i-1) cells of row r (see lattice3d_sig_kernel)
+                const uint32_t cb = pV[r] | 0x80008000u;
+                const uint32_t r0 = cb - ppV[r];                // -i
+                const uint32_t r1 = cb - pV[r - 1];             // -j
+                const uint32_t r2 = cb - pWm[r];                // -k
+                const uint32_t r3 = cb - W_ - 0x10001u;         // +i
+                const uint32_t r4 = cb - pV[r + 1] - 0x10001u;  // +j
+                const uint32_t r5 = cb - pWp[r] - 0x10001u;     // +k
+                const uint32_t u = ((r0 >> 15) & 0x10001u) + ((r1 >> 15) & 0x10001u) + ((r2 >> 15) & 0x10001u) +
+                                   ((r3 >> 15) & 0x10001u) + ((r4 >> 15) & 0x10001u) + ((r5 >> 15) & 0x10001u);
+                ev[r][4] = u * hs_pk + pV[r];
                 ppV[r] = pV[r];
                 pWm[r] = Wm[r];
                 pWp[r] = Wp;
@@ -566,6 +563,16 @@ __global__ void __launch_bounds__(256) lattice3d_rb_kernel(const typename Elem<D
             }
 #pragma unroll
             for (int r = 0; r < NR; ++r) pV[r] = V[r];
+            if (computes) {  // one divergent region per step (lanes 0 / 31 carry halos)
+#pragma unroll
+                for (int r = 1; r <= R; ++r) {
+                    inc2(hE, 0, hs, ev[r][0]);
+                    inc2(hE, 0, hs, ev[r][1]);
+                    inc2(hE, 0, hs, ev[r][2]);
+                    inc2(hV, 0, hs, ev[r][3]);
+                    inc2(hsig, 0, hs, ev[r][4]);
+                }
+            }
         };
         for (int s = 0; s < n; s += 2) {
             quant(s + 1, ra, V);  // plane t = s+1
