@@ -459,21 +459,23 @@ __global__ void __launch_bounds__(256) lattice3d_rb_kernel(const typename Elem<D
     char* hV = h + 8 * hs;
 
     const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x / 32;
     const bool computes = lane >= 1 && lane <= 30;
-    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x / 32);
-    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int Wi = (int)g.W, Di = (int)g.D;
     const int64_t plane_elems = g.W * g.D;
     const uint32_t sent4 = (uint32_t)(g.M + 1) * 4u;
     const uint32_t hs_pk = (uint32_t)hs;
     const int64_t per_chunk = (int64_t)g.tiles_j * g.tiles_k;
-    const int64_t it0 = g.n_items * gw / nwarps;
-    const int64_t it1 = g.n_items * (gw + 1) / nwarps;
 
-    for (int64_t item = it0; item < it1; ++item) {
+    // A CTA item is 8 vertically adjacent warp strips (8R lattice rows) x 60
+    // columns x a chunk of planes: the warps march the same planes in
+    // step, so the halo rows a warp shares with its neighbours are L1 hits.
+    // Items are strided over CTAs so that concurrently running CTAs hold
+    // adjacent column tiles and their halo columns meet in L2.
+    for (int64_t item = blockIdx.x; item < g.n_items; item += gridDim.x) {
         const int64_t ch = item / per_chunk;
         const int rem = (int)(item - ch * per_chunk);
-        const int j0 = (rem / g.tiles_k) * R;
+        const int j0 = (rem / g.tiles_k) * (8 * R) + warp * R;
         const int k0 = (rem % g.tiles_k) * 60;
         const int64_t ia = g.v0 + ch * g.chunk;
         const int64_t ib = min(ia + (int64_t)g.chunk, g.v1);
@@ -782,11 +784,11 @@ static int launch_l3(const ft_window* win, int64_t H, int64_t W, int64_t D, int6
         int per_sm = 0;
         FT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NTH, smem));
         if (per_sm < 1) return FT_ERR_ARG;
-        g.tiles_j = (int)cdiv(W + 1, R);
+        g.tiles_j = (int)cdiv(W + 1, (NTH / 32) * R);  // CTA items: 8 warp strips
         g.tiles_k = (int)cdiv(D + 1, 60);
         const int64_t grid_cap = (int64_t)nsm_l() * per_sm;
-        plan_items(g, (int64_t)g.tiles_j * g.tiles_k, 1, grid_cap * (NTH / 32), 32);
-        const int grid = (int)std::min<int64_t>(grid_cap, cdiv(g.n_items, NTH / 32));
+        plan_items(g, (int64_t)g.tiles_j * g.tiles_k, 1, grid_cap, 64);
+        const int grid = (int)std::min<int64_t>(grid_cap, g.n_items);
         kern<<<grid, NTH, smem, st>>>(static_cast<const T*>(win->data), g, qdev(qa),
                                       reinterpret_cast<unsigned long long*>(hist));
         FT_CUDA_TRY(cudaGetLastError());
