@@ -113,6 +113,27 @@ __device__ __forceinline__ uint32_t pack_pair(const typename Pair<DT>::T& v, boo
     return __byte_perm(a, b, 0x5410);
 }
 
+// float -> u16 with floor, saturating (PTX float-to-int conversions saturate).
+__device__ __forceinline__ uint32_t f2u16_rd(float f)
+{
+    unsigned short r;
+    asm("cvt.rmi.u16.f32 %0, %1;" : "=h"(r) : "f"(f));
+    return r;
+}
+
+// Packed-pair quantization for FT_Q_POW2: both cells converted with a
+// saturating floor to u16, then clamped to M, scaled to byte offsets and
+// masked to the sentinel as one 32-bit word (keep = 0xFFFF per present cell).
+template <int DT>
+__device__ __forceinline__ uint32_t pack_pair_pow2(const typename Pair<DT>::T& v, uint32_t keep, float scale,
+                                                   uint32_t Mpk, uint32_t sent2)
+{
+    const uint32_t a = f2u16_rd(__fmaf_rd((float)v.x, scale, 0.5f));
+    const uint32_t b = f2u16_rd(__fmaf_rd((float)v.y, scale, 0.5f));
+    const uint32_t w = __vminu2(__byte_perm(a, b, 0x5410), Mpk) << 2;
+    return (w & keep) | (sent2 & ~keep);
+}
+
 // Sum the CP copies of every (row, level) bin into the global histogram.
 template <int CP>
 __device__ __forceinline__ void flush_rows(uint32_t* h, unsigned long long* __restrict__ out, int nrows, int M2,
@@ -497,22 +518,30 @@ __global__ void __launch_bounds__(256) lattice3d_rb_kernel(const typename Elem<D
                 dst[r] = load_pair<DT, VEC>(at + r * Di, ok && okx, ok && oky);
             }
         };
+        const uint32_t lanekeep = (okx ? 0x0000FFFFu : 0u) | (oky ? 0xFFFF0000u : 0u);
         auto quant = [&](int t, const P2 (&src)[NR], uint32_t (&V)[NR]) {
             const bool pin = t >= t_lo && t < t_hi;
 #pragma unroll
             for (int r = 0; r < NR; ++r) {
                 const bool ok = pin && ((rowok >> r) & 1u);
-                V[r] = pack_pair<DT, QM, 0>(src[r], ok && okx, ok && oky, tt, q, g.M, sent4);
+                if constexpr (QM == FT_Q_POW2)
+                    V[r] = pack_pair_pow2<DT>(src[r], ok ? lanekeep : 0u, q.scale, (uint32_t)g.M * 0x10001u,
+                                              sent4 * 0x10001u);
+                else
+                    V[r] = pack_pair<DT, QM, 0>(src[r], ok && okx, ok && oky, tt, q, g.M, sent4);
             }
         };
 
-        uint32_t V[NR], pV[NR], ppV[NR], pWm[NR], pWp[NR], pm2k[NR], pm2j[NR], pm4i[NR];
+        uint32_t V[NR], pV[NR], tmi[NR], pWm[NR], pWp[NR], pm2k[NR], pm2j[NR], pm4i[NR];
         P2 ra[NR], rb[NR];
         // prologue: planes ia-2 (t = -1) and ia-1 (t = 0)
         fetch(-1, ptr, ra);
         fetch(0, ptr + plane_elems, rb);
-        quant(-1, ra, ppV);
+        quant(-1, ra, V);
         quant(0, rb, pV);
+        // "-i neighbour activates first" terms of the cells signed next: [V(ia-2) <= V(ia-1)]
+#pragma unroll
+        for (int r = 0; r < NR; ++r) tmi[r] = (((pV[r] | 0x80008000u) - V[r]) >> 15) & 0x10001u;
         fetch(1, ptr + 2 * plane_elems, ra);
         fetch(2, ptr + 3 * plane_elems, rb);
         ptr += 4 * plane_elems;  // next fetch: t = 3
@@ -531,7 +560,7 @@ __global__ void __launch_bounds__(256) lattice3d_rb_kernel(const typename Elem<D
         }
 
         auto step = [&]() {
-            uint32_t Wm[NR], ev[R + 1][5];
+            uint32_t Wm[NR], ev[R + 1][5], tpj = 0;
 #pragma unroll
             for (int r = 0; r < NR; ++r) Wm[r] = shift_pair(__shfl_up_sync(0xFFFFFFFFu, V[r], 1), V[r]);
 #pragma unroll
@@ -545,18 +574,20 @@ __global__ void __launch_bounds__(256) lattice3d_rb_kernel(const typename Elem<D
                 ev[r][1] = vmin2(m2k, pm2k[r]);  // edge along j
                 ev[r][2] = vmin2(m2j, pm2j[r]);  // edge along k
                 ev[r][3] = vmin2(m4i, pm4i[r]);  // vertex
-                // signature of the plane-(i-1) cells of row r (see lattice3d_sig_kernel)
+                // signature of the plane-(i-1) cells of row r (see lattice3d_sig_kernel).
+                // Each term is bit 15 / 31 of c' - n + k: "n activates before c".
+                // The -i term is the complement of the previous step's +i term and
+                // the -j term (rows >= 2) the complement of row r-1's +j term.
                 const uint32_t cb = pV[r] | 0x80008000u;
-                const uint32_t r0 = cb - ppV[r];                // -i
-                const uint32_t r1 = cb - pV[r - 1];             // -j
-                const uint32_t r2 = cb - pWm[r];                // -k
-                const uint32_t r3 = cb - W_ - 0x10001u;         // +i
-                const uint32_t r4 = cb - pV[r + 1] - 0x10001u;  // +j
-                const uint32_t r5 = cb - pWp[r] - 0x10001u;     // +k
-                const uint32_t u = ((r0 >> 15) & 0x10001u) + ((r1 >> 15) & 0x10001u) + ((r2 >> 15) & 0x10001u) +
-                                   ((r3 >> 15) & 0x10001u) + ((r4 >> 15) & 0x10001u) + ((r5 >> 15) & 0x10001u);
+                const uint32_t t1 = r == 1 ? ((cb - pV[0]) >> 15) & 0x10001u : 0x10001u - tpj;  // -j
+                const uint32_t t2 = ((cb - pWm[r]) >> 15) & 0x10001u;                             // -k
+                const uint32_t t3 = ((cb - W_ - 0x10001u) >> 15) & 0x10001u;                      // +i
+                const uint32_t t4 = ((cb - pV[r + 1] - 0x10001u) >> 15) & 0x10001u;               // +j
+                const uint32_t t5 = ((cb - pWp[r] - 0x10001u) >> 15) & 0x10001u;                  // +k
+                const uint32_t u = tmi[r] + t1 + t2 + t3 + t4 + t5;
                 ev[r][4] = u * hs_pk + pV[r];
-                ppV[r] = pV[r];
+                tmi[r] = 0x10001u - t3;
+                tpj = t4;
                 pWm[r] = Wm[r];
                 pWp[r] = Wp;
                 pm2k[r] = m2k;
