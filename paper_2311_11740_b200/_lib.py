@@ -7,6 +7,7 @@ or cannot be loaded, every entry point raises -- there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 
 from . import build as _build
@@ -41,6 +42,10 @@ def load(build_if_missing=True):
         if _lib is not None:
             return _lib
         path = _build.LIB
+        override = os.environ.get("FT_LIB")  # A/B experiments with alternative builds
+        if override:
+            path = type(path)(override)
+            build_if_missing = False
         if build_if_missing and not _build.up_to_date():
             try:
                 _build.build()

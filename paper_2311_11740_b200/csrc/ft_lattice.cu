@@ -460,7 +460,7 @@ __global__ void __launch_bounds__(SNT, 4) lattice3d_sig_kernel(const typename El
 // plane, two planes in flight), so there is no shared staging, no LDS/STS and
 // no CTA barrier: the shared memory serves only the histograms.
 template <int DT, int QM, bool VEC, int R>
-__global__ void __launch_bounds__(256) lattice3d_rb_kernel(const typename Elem<DT>::T* __restrict__ buf, LGeo g,
+__global__ void __launch_bounds__(256, 2) lattice3d_rb_kernel(const typename Elem<DT>::T* __restrict__ buf, LGeo g,
                                                            QuantDev q, unsigned long long* __restrict__ hist)
 {
     using P2 = typename Pair<DT>::T;
@@ -807,7 +807,9 @@ static int launch_l3(const ft_window* win, int64_t H, int64_t W, int64_t D, int6
     const bool vec3 = D % 2 == 0 && reinterpret_cast<uintptr_t>(win->data) % 8 == 0;
     static const char* which = getenv("FT_LATTICE_KERNEL");  // rb (default) | sig | staged
     if ((!which || !strcmp(which, "rb")) && 6 * (((M + 2) * 4 + 15) / 16 * 16) + (M + 1) * 4 < 0xFFFF) {
-        constexpr int R = 4, NTH = 256;
+        // R = 6 rows per warp strip: 127 registers, 2 CTAs/SM; measured at
+        // 2048^3: R=4 451, R=6 479, R=8 384 (spills), R=4 forced to 3 CTAs 440 Gvox/s
+        constexpr int R = 6, NTH = 256;
         g.hs = ((M + 2) * 4 + 15) / 16 * 16;
         const size_t smem = (size_t)9 * g.hs + (size_t)(M + 2) * 4;
         auto kern = vec3 ? lattice3d_rb_kernel<DT, QM, true, R> : lattice3d_rb_kernel<DT, QM, false, R>;
