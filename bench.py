@@ -120,12 +120,14 @@ def cpu_reference(x_host, M, lo_hi, descs, budget_s=15.0, threads=None):
             oracle.descriptor_numerators(q_in, q_out, M, w)
         return time.perf_counter() - t0
 
-    n = 2
+    # the oracle splits vertex rows over threads like the reference
+    # (_parallel.py:8-24): keep >= 4 planes per thread so all cores work
+    n = min(H, 4 * threads)
     t = run(n)
     while t < 0.5 and n < H:
-        n = min(H, n * 4)
+        n = min(H, n * 2)
         t = run(n)
-    n_final = max(1, min(H, int(n * budget_s / max(t, 1e-6))))
+    n_final = max(min(H, 4 * threads), min(H, int(n * budget_s / max(t, 1e-6))))
     t = run(n_final)
     cells = n_final * W * D
     return cells / t / 1e9, cells, t, threads
@@ -156,7 +158,7 @@ def main():
                           f"sigma={sigma:g} voxels, min-max normalised, {M + 1} levels; "
                           f"curves: {', '.join(descs)}",
               "field": [H, W, D], "sigma": sigma, "levels": M + 1, "descriptors": list(descs),
-              "partition": f"z-slabs over {ws} rank(s), 1-plane halo" + (", NCCL all-reduce" if ws > 1 else ""),
+              "partition": f"z-slabs over {ws} rank(s), 2 low halo planes" + (", NCCL all-reduce" if ws > 1 else ""),
               "l2": "inputs larger than L2 (field >> 126 MB)"}
 
     if args.impl == "reference":
@@ -360,7 +362,7 @@ def run_reference(args, shape, sigma, M, descs, config, ws):
     H, W, D = shape
     # same field bytes as our arm: generate on the GPU if present, else a CPU
     # stand-in of the same distribution; only a bounded slab is needed
-    nplanes = min(H, 64)
+    nplanes = min(H, max(64, 8 * (os.cpu_count() or 1)))
     if torch.cuda.is_available():
         x = synth.grf_slab(shape, sigma, args.seed, (0, nplanes), torch.device("cuda", 0))
         x = ((x - x.min()) / (x.max() - x.min())).cpu().numpy()

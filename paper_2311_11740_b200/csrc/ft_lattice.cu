@@ -747,6 +747,139 @@ __global__ void __launch_bounds__(L2W) lattice2d_kernel(const typename Elem<DT>:
     if (it0 < it1) flush_rows<CP>(reinterpret_cast<uint32_t*>(h), hist + cur_img * NR * M2, NR, M2, hs / 4, false);
 }
 
+// ------------------------------------------- 2D, register march + signatures
+// Same rows as lattice2d_kernel.  A 64-thread CTA (two warps, one shared
+// histogram set) owns 2 x 60 lattice columns of one image and a chunk of
+// rows; every lane marches its two k-adjacent cells down the rows with the
+// previous rows in registers and the j-neighbours one shuffle away (lanes 0
+// and 31 carry the halo columns).  Cells and edges are booked once per cell
+// (signature u = #edge neighbours that activate first under the reference's
+// row-major order, contrib2d.py:39-40: E = sum (4 - u) sig_u), vertices by
+// their min (and max for EC_4C): 2-3 shared atomics per lattice point.
+template <int DT, int QM, bool MAXES, bool VEC>
+__global__ void __launch_bounds__(64) lattice2d_rb_kernel(const typename Elem<DT>::T* __restrict__ buf, LGeo g,
+                                                          QuantDev q, unsigned long long* __restrict__ hist)
+{
+    using P2 = typename Pair<DT>::T;
+    using T = typename Elem<DT>::T;
+    constexpr int NR = 4;      // output rows: cells, edges, vertices, vertex maxes
+    constexpr int PF = 4;      // rows in flight per lane
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int M2 = g.M + 2;
+    const int hs = g.hs;
+    char* h = reinterpret_cast<char*>(smem_raw);  // rows: sig u = 0..4, vertices, vertex maxes
+    float* tt = reinterpret_cast<float*>(h + 7 * hs);
+    for (int i = threadIdx.x; i < 7 * hs / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(h)[i] = 0;
+    if (QM != FT_Q_IDENTITY && QM != FT_Q_POW2)
+        for (int i = threadIdx.x; i < M2; i += blockDim.x) tt[i] = q.tt[i];
+    __syncthreads();
+    char* hsig = h;
+    char* hV = h + 5 * hs;
+    char* hX = h + 6 * hs;
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool computes = lane >= 1 && lane <= 30;
+    const int Wi = (int)g.W;
+    const uint32_t sent4 = (uint32_t)(g.M + 1) * 4u;
+    const uint32_t hs_pk = (uint32_t)hs;
+
+    auto flush = [&](int64_t img, bool zero) {
+        __syncthreads();
+        uint32_t* hw = reinterpret_cast<uint32_t*>(h);
+        const int rw = hs / 4;
+        unsigned long long* out = hist + img * NR * M2;
+        for (int l = threadIdx.x; l < M2; l += blockDim.x) {
+            uint32_t c = 0, e = 0;
+#pragma unroll
+            for (int u = 0; u < 5; ++u) {
+                const uint32_t v = hw[u * rw + l];
+                c += v;
+                e += (4 - u) * v;
+                if (zero) hw[u * rw + l] = 0;
+            }
+            const uint32_t x = hw[5 * rw + l], y = hw[6 * rw + l];
+            if (zero) hw[5 * rw + l] = hw[6 * rw + l] = 0;
+            if (c) atomicAdd(&out[l], (unsigned long long)c);
+            if (e) atomicAdd(&out[M2 + l], (unsigned long long)e);
+            if (x) atomicAdd(&out[2 * M2 + l], (unsigned long long)x);
+            if (y) atomicAdd(&out[3 * M2 + l], (unsigned long long)y);
+        }
+        __syncthreads();
+    };
+
+    int64_t cur_img = -1;
+    for (int64_t item = blockIdx.x; item < g.n_items; item += gridDim.x) {
+        const int64_t b = item / g.items_per_image;
+        if (b != cur_img) {
+            if (cur_img >= 0) flush(cur_img, true);
+            cur_img = b;
+        }
+        const int64_t rem = item - b * g.items_per_image;
+        const int64_t ch = rem / g.tiles_k;
+        const int k0 = (int)(rem % g.tiles_k) * 120 + warp * 60;
+        const int64_t ia = g.v0 + ch * g.chunk;
+        const int64_t ib = min(ia + (int64_t)g.chunk, g.v1);
+        const int kk = k0 - 2 + 2 * lane;
+        const bool okx = kk >= 0 && kk < Wi, oky = kk >= 0 && kk + 1 < Wi;
+        const uint32_t lanekeep = (okx ? 0x0000FFFFu : 0u) | (oky ? 0xFFFF0000u : 0u);
+        const int n = (int)(ib - ia);
+        const int t_lo = (int)max((int64_t)-1, 1 - ia);
+        const int t_hi = (int)min((int64_t)(n + 2), g.H - ia + 1);
+        const T* ptr = buf + b * g.bstride + ((ia - 2 - g.first) * g.W + (okx ? kk : 0));
+        auto fetch = [&](int t) {
+            const bool pin = t >= t_lo && t < t_hi;
+            return load_pair<DT, VEC>(ptr + (int64_t)(t + 1) * g.W, pin && okx, pin && oky);
+        };
+        auto quant = [&](int t, const P2& v) -> uint32_t {
+            const bool pin = t >= t_lo && t < t_hi;
+            if constexpr (QM == FT_Q_POW2)
+                return pack_pair_pow2<DT>(v, pin ? lanekeep : 0u, q.scale, (uint32_t)g.M * 0x10001u,
+                                          sent4 * 0x10001u);
+            else
+                return pack_pair<DT, QM, 0>(v, pin && okx, pin && oky, tt, q, g.M, sent4);
+        };
+        // rows relative to ia-1: t = -1 .. n (row ia-1+t)
+        const uint32_t r_m1 = quant(-1, fetch(-1));
+        uint32_t pW = quant(0, fetch(0));  // row ia-1
+        P2 raw[PF];
+#pragma unroll
+        for (int p = 0; p < PF; ++p) raw[p] = fetch(1 + p);
+        uint32_t pWm = shift_pair(__shfl_up_sync(0xFFFFFFFFu, pW, 1), pW);
+        uint32_t pWp = shift_pair(pW, __shfl_down_sync(0xFFFFFFFFu, pW, 1));
+        uint32_t tmi = (((pW | 0x80008000u) - r_m1) >> 15) & 0x10001u;  // [row ia-2 <= row ia-1]
+
+        for (int s0 = 0; s0 < n; s0 += PF) {
+#pragma unroll
+            for (int p = 0; p < PF; ++p) {
+                const int s = s0 + p;
+                if (s >= n) break;
+                const uint32_t W_ = quant(s + 1, raw[p]);
+                if (s + PF < n) raw[p] = fetch(s + 1 + PF);
+                const uint32_t Wm = shift_pair(__shfl_up_sync(0xFFFFFFFFu, W_, 1), W_);
+                const uint32_t Wp = shift_pair(W_, __shfl_down_sync(0xFFFFFFFFu, W_, 1));
+                const uint32_t ev = vmin2(W_, Wm);                 // edge (i,j)-(i+1,j)
+                const uint32_t vx = vmin2(ev, vmin2(pW, pWm));     // vertex
+                // signature of the row-(i-1) cells pW
+                const uint32_t cb = pW | 0x80008000u;
+                const uint32_t t_mj = ((cb - pWm) >> 15) & 0x10001u;             // -j
+                const uint32_t t_pj = ((cb - pWp - 0x10001u) >> 15) & 0x10001u;  // +j
+                const uint32_t t_pi = ((cb - W_ - 0x10001u) >> 15) & 0x10001u;   // +i
+                const uint32_t u = tmi + t_mj + t_pj + t_pi;
+                if (computes) {
+                    inc2(hsig, 0, hs, u * hs_pk + pW);
+                    inc2(hV, 0, hs, vx);
+                    if constexpr (MAXES) inc2(hX, 0, hs, vmax2(vmax2(W_, Wm), vmax2(pW, pWm)));
+                }
+                tmi = 0x10001u - t_pi;
+                pW = W_;
+                pWm = Wm;
+                pWp = Wp;
+            }
+        }
+    }
+    if (cur_img >= 0) flush(cur_img, false);
+}
+
 static int nsm_l()
 {
     int dev = 0, n = kSMs;
@@ -894,6 +1027,33 @@ static int launch_l2(const ft_window* win, int64_t H, int64_t W, int64_t v0, int
     const size_t smem = (size_t)4 * g.hs + (size_t)(M + 2) * 4 + 2 * L2W * 4;
     const bool vec = W % 2 == 0 && (batch <= 1 || win->batch_stride % 2 == 0) &&
                      reinterpret_cast<uintptr_t>(win->data) % 8 == 0;
+    static const char* which = getenv("FT_LATTICE_KERNEL");  // rb (default) | staged
+    const int hs_rb = ((M + 2) * 4 + 15) / 16 * 16;
+    if ((!which || !strcmp(which, "rb")) && 4 * hs_rb + (M + 1) * 4 < 0xFFFF) {
+        g.hs = hs_rb;
+        const size_t smem_rb = (size_t)7 * hs_rb + (size_t)(M + 2) * 4;
+        using K = void (*)(const T*, LGeo, QuantDev, unsigned long long*);
+        K kern = maxes ? (vec ? lattice2d_rb_kernel<DT, QM, true, true> : lattice2d_rb_kernel<DT, QM, true, false>)
+                       : (vec ? lattice2d_rb_kernel<DT, QM, false, true> : lattice2d_rb_kernel<DT, QM, false, false>);
+        FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rb));
+        int per_sm = 0;
+        FT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 64, smem_rb));
+        if (per_sm < 1) return FT_ERR_ARG;
+        g.tiles_k = (int)cdiv(W + 1, 120);
+        const int64_t grid_cap = (int64_t)nsm_l() * per_sm;
+        // about one item per CTA (equal work), marches of >= 64 rows
+        const int64_t rows = v1 - v0;
+        int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>(cdiv(grid_cap, g.tiles_k * batch), rows / 64));
+        g.chunk = (int)cdiv(rows, nchunks);
+        nchunks = cdiv(rows, g.chunk);
+        g.items_per_image = g.tiles_k * nchunks;
+        g.n_items = g.items_per_image * batch;
+        const int grid = (int)std::min<int64_t>(grid_cap, g.n_items);
+        kern<<<grid, 64, smem_rb, st>>>(static_cast<const T*>(win->data), g, qdev(qa),
+                                        reinterpret_cast<unsigned long long*>(hist));
+        FT_CUDA_TRY(cudaGetLastError());
+        return FT_OK;
+    }
     using K = void (*)(const T*, LGeo, QuantDev, unsigned long long*);
     K kern;
     if (maxes) {

@@ -1,11 +1,12 @@
 """Profiling driver: build a synthetic field on cuda:0 and launch the hot
 kernels a few times (for ncu / timing).
-    python tools/prof_run.py [c4a|c5|small] [reps] [map|lattice|both]"""
+    python tools/prof_run.py [c4a|c5|small|c2|c3] [reps] [map|lattice|both]"""
 import sys
 import time
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2311_11740_b200 as ft  # noqa: E402
@@ -14,21 +15,40 @@ from paper_2311_11740_b200 import engine, synth  # noqa: E402
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c4a"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 kind = sys.argv[3] if len(sys.argv) > 3 else "both"
-shape, sigma, M = {"c4a": ((512, 512, 512), 3.0, 255), "c5": ((2048, 2048, 2048), 4.0, 511),
-                   "small": ((256, 256, 256), 3.0, 255)}[cfg]
 dev = torch.device("cuda", 0)
-x = synth.grf_slab(shape, sigma, 2311, (0, shape[0]), dev)
-synth.normalise_(x, x.min(), x.max())
-q = ft.quant.QuantSpec.for_range(0.0, 1.0, M)
+batch, bstride = 1, 0
+if cfg in ("c4a", "c5", "small"):
+    shape, sigma, M = {"c4a": ((512, 512, 512), 3.0, 255), "c5": ((2048, 2048, 2048), 4.0, 511),
+                       "small": ((256, 256, 256), 3.0, 255)}[cfg]
+    x = synth.grf_slab(shape, sigma, 2311, (0, shape[0]), dev)
+    synth.normalise_(x, x.min(), x.max())
+    q = ft.quant.QuantSpec.for_range(0.0, 1.0, M)
+elif cfg == "c2":
+    shape, M = (8192, 8192), 255
+    x = synth.grf_2d(shape, 4.0, 2311, dev)
+    synth.normalise_(x, x.min(), x.max())
+    q = ft.quant.QuantSpec.for_range(0.0, 1.0, M)
+else:  # c3: 512 microscopy-like u8 images, 1024^2, sigma ~ U[1, 8]
+    shape, M, batch = (1024, 1024), 255, 512
+    sig = np.random.default_rng(2311).uniform(1.0, 8.0, batch)
+    x = torch.empty((batch,) + shape, dtype=torch.uint8, device=dev)
+    for b in range(batch):
+        im = synth.grf_2d(shape, float(sig[b]), 2311 + b, dev)
+        im = (im - im.min()) / (im.max() - im.min())
+        x[b] = torch.floor(im * 255 + 0.5).to(torch.uint8)
+    bstride = shape[0] * shape[1]
+    q = ft.quant.QuantSpec.identity()
+ndim = len(shape)
+cells = x.numel()
 torch.cuda.synchronize()
 for name in (("map", "lattice") if kind == "both" else (kind,)):
-    h = engine.new_hist(3, M, dev) if name == "map" else engine.new_lattice_hist(3, M, dev)
-    launch = engine.launch_hist if name == "map" else engine.launch_lattice
     for r in range(reps):
-        h.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        launch(3, x, shape, M, q, hist=h)
+        if name == "map":
+            engine.launch_hist(ndim, x, shape, M, q, batch=batch, batch_stride=bstride)
+        else:
+            engine.launch_lattice(ndim, x, shape, M, q, batch=batch, batch_stride=bstride)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
-        print(f"{cfg} {name} rep {r}: {dt * 1e3:.3f} ms  {x.numel() / dt / 1e9:.1f} Gvox/s")
+        print(f"{cfg} {name} rep {r}: {dt * 1e3:.3f} ms  {cells / dt / 1e9:.1f} Gvox/s")
