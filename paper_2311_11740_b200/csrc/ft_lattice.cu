@@ -782,6 +782,7 @@ __global__ void __launch_bounds__(64) lattice2d_rb_kernel(const typename Elem<DT
     const int Wi = (int)g.W;
     const uint32_t sent4 = (uint32_t)(g.M + 1) * 4u;
     const uint32_t hs_pk = (uint32_t)hs;
+    const uint32_t halo4 = computes ? 0u : sent4 * 0x10001u;
 
     auto flush = [&](int64_t img, bool zero) {
         __syncthreads();
@@ -830,8 +831,8 @@ __global__ void __launch_bounds__(64) lattice2d_rb_kernel(const typename Elem<DT
             const bool pin = t >= t_lo && t < t_hi;
             return load_pair<DT, VEC>(ptr + (int64_t)(t + 1) * g.W, pin && okx, pin && oky);
         };
-        auto quant = [&](int t, const P2& v) -> uint32_t {
-            const bool pin = t >= t_lo && t < t_hi;
+        auto quant = [&](int t, const P2& v, bool inside) -> uint32_t {
+            const bool pin = inside || (t >= t_lo && t < t_hi);
             if constexpr (QM == FT_Q_POW2)
                 return pack_pair_pow2<DT>(v, pin ? lanekeep : 0u, q.scale, (uint32_t)g.M * 0x10001u,
                                           sent4 * 0x10001u);
@@ -839,8 +840,8 @@ __global__ void __launch_bounds__(64) lattice2d_rb_kernel(const typename Elem<DT
                 return pack_pair<DT, QM, 0>(v, pin && okx, pin && oky, tt, q, g.M, sent4);
         };
         // rows relative to ia-1: t = -1 .. n (row ia-1+t)
-        const uint32_t r_m1 = quant(-1, fetch(-1));
-        uint32_t pW = quant(0, fetch(0));  // row ia-1
+        const uint32_t r_m1 = quant(-1, fetch(-1), false);
+        uint32_t pW = quant(0, fetch(0), false);  // row ia-1
         P2 raw[PF];
 #pragma unroll
         for (int p = 0; p < PF; ++p) raw[p] = fetch(1 + p);
@@ -848,32 +849,47 @@ __global__ void __launch_bounds__(64) lattice2d_rb_kernel(const typename Elem<DT
         uint32_t pWp = shift_pair(pW, __shfl_down_sync(0xFFFFFFFFu, pW, 1));
         uint32_t tmi = (((pW | 0x80008000u) - r_m1) >> 15) & 0x10001u;  // [row ia-2 <= row ia-1]
 
-        for (int s0 = 0; s0 < n; s0 += PF) {
+        // One lattice row.  The halo lanes 0 and 31 book into the sentinel
+        // bin M+1 (never read: curves stop at level M) instead of branching.
+        auto step = [&](uint32_t W_) {
+            const uint32_t Wm = shift_pair(__shfl_up_sync(0xFFFFFFFFu, W_, 1), W_);
+            const uint32_t Wp = shift_pair(W_, __shfl_down_sync(0xFFFFFFFFu, W_, 1));
+            const uint32_t ev = vmin2(W_, Wm);              // edge (i,j)-(i+1,j)
+            const uint32_t vx = vmin2(ev, vmin2(pW, pWm));  // vertex
+            // signature of the row-(i-1) cells pW
+            const uint32_t cb = pW | 0x80008000u;
+            const uint32_t t_mj = ((cb - pWm) >> 15) & 0x10001u;             // -j
+            const uint32_t t_pj = ((cb - pWp - 0x10001u) >> 15) & 0x10001u;  // +j
+            const uint32_t t_pi = ((cb - W_ - 0x10001u) >> 15) & 0x10001u;   // +i
+            const uint32_t u = tmi + t_mj + t_pj + t_pi;
+            inc2(hsig, 0, hs, u * hs_pk + vmax2(pW, halo4));
+            inc2(hV, 0, hs, vmax2(vx, halo4));
+            if constexpr (MAXES) inc2(hX, 0, hs, vmax2(vmax2(W_, Wm), vmax2(vmax2(pW, pWm), halo4)));
+            tmi = 0x10001u - t_pi;
+            pW = W_;
+            pWm = Wm;
+            pWp = Wp;
+        };
+        // steady state: every row fetched and quantized is inside the image
+        const int S = min(n - PF, t_hi - 1 - PF);
+        int s0 = 0;
+        for (; s0 + PF <= S; s0 += PF) {
+#pragma unroll
+            for (int p = 0; p < PF; ++p) {
+                const int s = s0 + p;
+                const uint32_t W_ = quant(s + 1, raw[p], true);
+                raw[p] = load_pair<DT, VEC>(ptr + (int64_t)(s + 2 + PF) * g.W, okx, oky);
+                step(W_);
+            }
+        }
+        for (; s0 < n; s0 += PF) {
 #pragma unroll
             for (int p = 0; p < PF; ++p) {
                 const int s = s0 + p;
                 if (s >= n) break;
-                const uint32_t W_ = quant(s + 1, raw[p]);
+                const uint32_t W_ = quant(s + 1, raw[p], false);
                 if (s + PF < n) raw[p] = fetch(s + 1 + PF);
-                const uint32_t Wm = shift_pair(__shfl_up_sync(0xFFFFFFFFu, W_, 1), W_);
-                const uint32_t Wp = shift_pair(W_, __shfl_down_sync(0xFFFFFFFFu, W_, 1));
-                const uint32_t ev = vmin2(W_, Wm);                 // edge (i,j)-(i+1,j)
-                const uint32_t vx = vmin2(ev, vmin2(pW, pWm));     // vertex
-                // signature of the row-(i-1) cells pW
-                const uint32_t cb = pW | 0x80008000u;
-                const uint32_t t_mj = ((cb - pWm) >> 15) & 0x10001u;             // -j
-                const uint32_t t_pj = ((cb - pWp - 0x10001u) >> 15) & 0x10001u;  // +j
-                const uint32_t t_pi = ((cb - W_ - 0x10001u) >> 15) & 0x10001u;   // +i
-                const uint32_t u = tmi + t_mj + t_pj + t_pi;
-                if (computes) {
-                    inc2(hsig, 0, hs, u * hs_pk + pW);
-                    inc2(hV, 0, hs, vx);
-                    if constexpr (MAXES) inc2(hX, 0, hs, vmax2(vmax2(W_, Wm), vmax2(pW, pWm)));
-                }
-                tmi = 0x10001u - t_pi;
-                pW = W_;
-                pWm = Wm;
-                pWp = Wp;
+                step(W_);
             }
         }
     }

@@ -2,7 +2,6 @@
 kernels a few times (for ncu / timing).
     python tools/prof_run.py [c4a|c5|small|c2|c3] [reps] [map|lattice|both]"""
 import sys
-import time
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
@@ -44,11 +43,13 @@ torch.cuda.synchronize()
 for name in (("map", "lattice") if kind == "both" else (kind,)):
     for r in range(reps):
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
         if name == "map":
             engine.launch_hist(ndim, x, shape, M, q, batch=batch, batch_stride=bstride)
         else:
             engine.launch_lattice(ndim, x, shape, M, q, batch=batch, batch_stride=bstride)
+        e1.record()
         torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
+        dt = e0.elapsed_time(e1) / 1e3  # launches go to torch's current stream
         print(f"{cfg} {name} rep {r}: {dt * 1e3:.3f} ms  {cells / dt / 1e9:.1f} Gvox/s")
