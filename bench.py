@@ -142,6 +142,8 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c5")
     ap.add_argument("--seed", type=int, default=2311)
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--kernel", choices=("lines", "lattice"), default="lines",
+                    help="fused curve kernel (A/B): ft_lines3d (default) or ft_lattice3d")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
@@ -193,19 +195,23 @@ def main():
     quant = ft.quant.QuantSpec.for_range(0.0, 1.0, M)
     tables = [ft.builtin_weights(d, "26C") for d in descs]
     eighths = [t.eighths for t in tables]
-    row_w = np.array([ft.lattice.row_weights(3, tuple(e))[0] for e in eighths], np.int64)
-    hist = engine.new_lattice_hist(3, M, dev)
+    plan = ft.lattice.fused_plan(3, eighths, lines_ok=args.kernel == "lines" and engine.lines_ok(M))
+    kind = ft.gather.Kind(plan[0], plan[1])
+    row_w = plan[2]
+    kname = {"lines": "lines3d_kernel (line-decomposition EC / surface / volume histograms)",
+             "lattice": "lattice3d_rb_kernel (element min-filter histograms)"}[plan[0]]
+    hist = kind.new(3, M, dev)
     stream = torch.cuda.current_stream(dev)
     k_start, k_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     kernel_ms = []
 
     def step(timed_kernel=False):
-        # the fused curve path: element histograms (ft_lattice3d) -> NCCL
+        # the fused curve path: level histograms (ft_lines3d) -> NCCL
         # all-reduce (N > 1) -> device prefix scan into the three curves
         hist.zero_()
         if timed_kernel:
             k_start.record(stream)
-        engine.launch_lattice(3, x, shape, M, quant, rows=(a, b), first=r0, hist=hist)
+        kind.launch(3, x, shape, M, quant, (a, b), first=r0, hist=hist)
         if timed_kernel:
             k_end.record(stream)
         if ws > 1:
@@ -267,7 +273,6 @@ def main():
         del x
         torch.cuda.empty_cache()
         src = ft.ArraySource(host, M, value_range=(0.0, 1.0))  # pinned: H2D straight from its pages
-        lattice_kind = ft.gather.Kind("lattice")
         e_times = []
         for it in range(1 + e2e_steps):
             barrier()
@@ -280,7 +285,7 @@ def main():
             else:
                 # the rank's planes [r0, r1) stand for global planes
                 h = ft.gather.stream_hist(_ShiftedSource(src, r0, H), 3, dev, (a, b), chunk_bytes=512 << 20,
-                                          kind=lattice_kind)
+                                          kind=kind)
                 import torch.distributed as dist
                 dist.all_reduce(h)
                 curves = engine.curves_from_rows(h, M, row_w).cpu().numpy()
@@ -319,7 +324,7 @@ def main():
                "config": config,
                "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                             "frac": round(achieved / peak, 4), "traffic": None,
-                            "kernel": "lattice3d_kernel (fused curve histograms), per-launch median over CUDA events",
+                            "kernel": kname + ", per-launch median over CUDA events",
                             "kernel_ms": round(kms, 4), "peak_source": peak_kind,
                             "algorithmic_bytes_per_launch": int(bytes_per_launch)},
                "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": 2 * args.steps,

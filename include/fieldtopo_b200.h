@@ -114,6 +114,19 @@ int ft_lattice3d(const ft_window *win, int64_t H, int64_t W, int64_t D, int64_t 
 int ft_lattice2d(const ft_window *win, int64_t H, int64_t W, int64_t v0, int64_t v1,
                  const ft_quant *q, int32_t M, int32_t maxes, uint64_t *hist, void *stream);
 
+/* Fused curve path for 3D EC / surface-area / volume (ft_lines.cu): the same
+ * counts as ft_lattice3d folded into three rows, with ~2.6 instead of 10
+ * shared-memory events per lattice point (EC by 1D extremum events along i of
+ * four min-derived line families, cubes and faces by per-cell signatures;
+ * DESIGN.md §3e).  hist: device uint64 [3][M+2], accumulated: cells C,
+ * faces F, and X = V - E (two's complement, may be negative), so
+ * EC_26C = X + F - C, surface area = 2F - 6C, volume = C; tables outside
+ * span{C, F, V - E} need ft_lattice3d.  Window as ft_lattice3d (planes
+ * v0-2 .. v1-1).  Requires ft_lines3d_ok(M) (M <= ~2300). */
+int ft_lines3d(const ft_window *win, int64_t H, int64_t W, int64_t D, int64_t v0, int64_t v1,
+               const ft_quant *q, int32_t M, uint64_t *hist, void *stream);
+int ft_lines3d_ok(int32_t M);
+
 /* Transition histograms -> contribution maps and descriptor curves.
  * hist [batch][C][M+2] (C = 6 or 40).  q_in / q_out (may be NULL): device
  * uint64 [batch][T][M+2], OVERWRITTEN with the reference maps

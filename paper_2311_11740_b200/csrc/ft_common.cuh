@@ -45,6 +45,7 @@ struct QuantDev {
     int negate;      // reversed range (hi < lo): evaluate on -x
     float scale, bias;
     const float* tt; // device, M+2 entries (kernels stage a shared copy)
+    float inv;       // FT_Q_POW2: 1 / hi (exact, a power of two), set per launch
 };
 
 template <int DT, int QM>

@@ -91,13 +91,13 @@ def descriptor_curves_distributed(x, shape, max_level, tables, value_range=None,
     M = int(max_level)
     quant = QuantSpec.for_range(*value_range, M) if value_range is not None else QuantSpec.identity()
     tables = list(tables)
-    rw = [lattice.row_weights(ndim, tuple(int(e) for e in t.eighths)) for t in tables]
-    use_lattice = all(r is not None for r in rw) and engine.lattice_ok(ndim, shape, M)
-    if use_lattice:
-        maxes = ndim == 2 and any(lattice.needs_max_rows(r[0]) for r in rw)
-        hist = all_reduce_hist(local_hist(ndim, x, shape, slab, M, quant, gather.Kind("lattice", maxes)), group)
-        num = engine.curves_from_rows(hist, M, np.array([r[0] for r in rw])).cpu().numpy()
-        num = num // np.array([r[1] for r in rw])[:, None]
+    plan = None
+    if engine.lattice_ok(ndim, shape, M):
+        plan = lattice.fused_plan(ndim, [t.eighths for t in tables], lines_ok=ndim == 3 and engine.lines_ok(M))
+    if plan is not None:
+        hist = all_reduce_hist(local_hist(ndim, x, shape, slab, M, quant, gather.Kind(plan[0], plan[1])), group)
+        num = engine.curves_from_rows(hist, M, plan[2]).cpu().numpy()
+        num = num // plan[3][:, None]
     else:
         hist = all_reduce_hist(local_hist(ndim, x, shape, slab, M, quant), group)
         _, _, num = engine.finalize(ndim, M, hist, maps=False, tables=[t.eighths for t in tables])

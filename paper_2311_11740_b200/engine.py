@@ -139,6 +139,33 @@ def launch_lattice(ndim, x, shape, M, quant, rows=None, first=0, hist=None, batc
     return hist
 
 
+def new_lines_hist(M, device):
+    return torch().zeros((3, M + 2), dtype=torch().int64, device=device)
+
+
+def launch_lines(x, shape, M, quant, rows=None, first=0, hist=None):
+    """Accumulate the 3D line-decomposition rows (C, F, V - E; ft_lines3d) of
+    lattice rows ``rows`` = [v0, v1); arguments as ``launch_hist``."""
+    L = _lib.load()
+    dev = x.device
+    H = shape[0]
+    v0, v1 = rows if rows is not None else (0, H + 1)
+    if hist is None:
+        hist = new_lines_hist(M, dev)
+    win = _lib.ft_window(ctypes.c_void_p(x.data_ptr()), dtype_code(x), int(first), int(x.shape[0]), 1, 0)
+    qs, keep = device_struct(quant, dev)
+    rc = L.ft_lines3d(ctypes.byref(win), H, shape[1], shape[2], v0, v1, ctypes.byref(qs), M,
+                      ctypes.c_void_p(hist.data_ptr()), _stream_ptr(dev))
+    del keep
+    _lib.check(rc, "ft_lines3d")
+    return hist
+
+
+def lines_ok(M):
+    """Whether ft_lines3d takes this level count (16-bit packed row offsets)."""
+    return bool(_lib.load().ft_lines3d_ok(int(M)))
+
+
 def lattice_ok(ndim, shape, M, x=None):
     """Whether the fused lattice kernels accept this field (levels * 4 must
     fit the 16-bit packed lanes)."""

@@ -18,7 +18,8 @@ _parallel.py:8-33) with:
 
 ``kind`` selects the kernel family: "map" = transition-class histograms
 (ft_hist2d/3d -> contribution maps), "lattice" = element histograms
-(ft_lattice2d/3d -> curves only).  Every path gives the same histogram bit
+(ft_lattice2d/3d -> curves only), "lines" = the 3D line-decomposition rows
+(ft_lines3d -> EC / surface-area / volume curves only).  Every path gives the same histogram bit
 for bit: integer sums commute.
 """
 
@@ -42,12 +43,16 @@ class Kind:
     def new(self, ndim, M, device, batch=1):
         if self.name == "map":
             return engine.new_hist(ndim, M, device, batch)
+        if self.name == "lines":
+            return engine.new_lines_hist(M, device)
         return engine.new_lattice_hist(ndim, M, device, batch)
 
     def launch(self, ndim, x, shape, M, quant, rows, first=0, hist=None, batch=1, batch_stride=0):
         if self.name == "map":
             return engine.launch_hist(ndim, x, shape, M, quant, rows=rows, first=first, hist=hist, batch=batch,
                                       batch_stride=batch_stride)
+        if self.name == "lines":
+            return engine.launch_lines(x, shape, M, quant, rows=rows, first=first, hist=hist)
         return engine.launch_lattice(ndim, x, shape, M, quant, rows=rows, first=first, hist=hist, batch=batch,
                                      batch_stride=batch_stride, maxes=self.maxes)
 

@@ -32,6 +32,8 @@ _V3 = np.full(21, 8)
 _F3 = (_SA3 + 6 * _C3) // 2
 _E3 = _V3 + _F3 - _C3 - _EC3
 BASIS_3D = np.stack([_C3, _F3, _E3, _V3])          # rows: C, F, E, V
+# rows of the line-decomposition kernel (ft_lines3d): C, F, X = V - E
+BASIS_3D_LINES = np.stack([_C3, _F3, _V3 - _E3])
 
 # E_max is not needed: per edge [min <= l] + [max <= l] = [a <= l] + [b <= l],
 # so E + E_max = 4 C and EC_4C = C - E_max + V_max = -3 C + E + V_max.
@@ -75,10 +77,16 @@ def _solve_exact(basis, w):
 
 
 @lru_cache(maxsize=256)
-def row_weights(ndim, eighths):
+def row_weights(ndim, eighths, rows="lattice"):
     """(integer row weights, divisor d) such that the table's curve
-    numerators are cumsum(sum_X w_X H_X) / d; None if not expressible."""
-    basis = BASIS_3D if ndim == 3 else BASIS_2D
+    numerators are cumsum(sum_X w_X H_X) / d; None if not expressible.
+    ``rows``: "lattice" (ft_lattice2d/3d rows) or "lines" (ft_lines3d rows)."""
+    if rows == "lines":
+        basis = BASIS_3D_LINES if ndim == 3 else None
+        if basis is None:
+            return None
+    else:
+        basis = BASIS_3D if ndim == 3 else BASIS_2D
     c = _solve_exact(basis, eighths)
     if c is None:
         return None
@@ -95,3 +103,19 @@ def needs_max_rows(weights):
 
 
 N_ROWS = {2: 4, 3: 4}
+
+
+def fused_plan(ndim, tables_eighths, lines_ok=True):
+    """Kernel choice for the fused curve path: ("lines" | "lattice", maxes,
+    int64 row weights [n_tables, n_rows], divisors [n_tables]), or None when a
+    table is outside the span of every fused kernel (the map path then)."""
+    keys = [tuple(int(e) for e in t) for t in tables_eighths]
+    if ndim == 3 and lines_ok:
+        rw = [row_weights(3, k, "lines") for k in keys]
+        if all(r is not None for r in rw):
+            return "lines", False, np.array([r[0] for r in rw], np.int64), np.array([r[1] for r in rw], np.int64)
+    rw = [row_weights(ndim, k) for k in keys]
+    if any(r is None for r in rw):
+        return None
+    maxes = ndim == 2 and any(needs_max_rows(r[0]) for r in rw)
+    return "lattice", maxes, np.array([r[0] for r in rw], np.int64), np.array([r[1] for r in rw], np.int64)

@@ -1,0 +1,12 @@
+// Dev harness: instantiate ONE lines3d_kernel variant for fast ptxas / SASS checks.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include -Xptxas -v -cubin tools/dev/lines_one.cu
+#define FT_DEV_KERNEL_ONLY
+#include "../../paper_2311_11740_b200/csrc/ft_lines.cu"
+#ifndef DEV_FOLD
+#define DEV_FOLD true
+#endif
+#ifndef DEV_GUARD
+#define DEV_GUARD false
+#endif
+template __global__ void ft::lines3d_kernel<FT_F32, FT_Q_POW2, true, ft::LINES_R, DEV_FOLD, DEV_GUARD>(const float*, ft::LGeo, ft::QuantDev,
+                                                                                   unsigned long long*);

@@ -1,0 +1,34 @@
+"""Build A/B variants of ft_lines.cu (F32 / FT_Q_POW2 path only) linked with the
+other objects of the main build:  python tools/dev/variants.py name="-DX=1 -DY=2" ...
+Each lands in variants/<name>/libfieldtopo_b200.so (use with FT_LIB=...)."""
+import concurrent.futures as cf
+import subprocess
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[2]
+sys.path.insert(0, str(ROOT))
+from paper_2311_11740_b200 import build as b  # noqa: E402
+
+objs = [p for p in sorted(b.BUILD.glob("*.o")) if p.stem != "ft_lines"]
+
+
+def one(spec):
+    name, flags = spec.split("=", 1)
+    out = ROOT / "variants" / name
+    out.mkdir(parents=True, exist_ok=True)
+    obj = out / "ft_lines.o"
+    cmd = [b.nvcc(), *b.ARCH, *b.NVCC_FLAGS, "-DFT_LINES_F32_ONLY", *flags.split(), "-Xptxas", "-v", "-c",
+           str(b.CSRC / "ft_lines.cu"), "-o", str(obj)]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode:
+        return f"{name}: FAILED\n{r.stderr[-2000:]}"
+    info = [l for l in r.stderr.splitlines() if "registers" in l or "spill" in l]
+    r2 = subprocess.run([b.nvcc(), *b.ARCH, "-shared", "-o", str(out / "libfieldtopo_b200.so"), str(obj),
+                         *map(str, objs)], capture_output=True, text=True)
+    return f"{name}: {'ok' if not r2.returncode else r2.stderr[-500:]}  " + " | ".join(info[-4:])
+
+
+with cf.ThreadPoolExecutor(8) as ex:
+    for line in ex.map(one, sys.argv[1:]):
+        print(line)

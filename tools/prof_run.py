@@ -1,6 +1,6 @@
 """Profiling driver: build a synthetic field on cuda:0 and launch the hot
 kernels a few times (for ncu / timing).
-    python tools/prof_run.py [c4a|c5|small|c2|c3] [reps] [map|lattice|both]"""
+    python tools/prof_run.py [c4a|c5|small|c2|c3] [reps] [map|lattice|lines|both|all]"""
 import sys
 from pathlib import Path
 
@@ -40,13 +40,18 @@ else:  # c3: 512 microscopy-like u8 images, 1024^2, sigma ~ U[1, 8]
 ndim = len(shape)
 cells = x.numel()
 torch.cuda.synchronize()
-for name in (("map", "lattice") if kind == "both" else (kind,)):
+names = {"both": ("map", "lattice"), "all": ("map", "lattice", "lines")}.get(kind, (kind,))
+for name in names:
+    if name == "lines" and ndim != 3:
+        continue
     for r in range(reps):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         if name == "map":
             engine.launch_hist(ndim, x, shape, M, q, batch=batch, batch_stride=bstride)
+        elif name == "lines":
+            engine.launch_lines(x, shape, M, q)
         else:
             engine.launch_lattice(ndim, x, shape, M, q, batch=batch, batch_stride=bstride)
         e1.record()
