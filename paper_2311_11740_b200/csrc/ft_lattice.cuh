@@ -22,6 +22,8 @@ struct LGeo {
     int M, tiles_j, tiles_k, chunk, hs;
     int64_t n_items, items_per_image;
     int ti_j0, ti_j1, ti_k0, ti_k1;  // ft_lines3d: interior tile ranges (guard-free kernel)
+    int hk;                          // ft_lines3d: signature row stride / 255
+    int rf_n, rf_j0[4];              // ft_lines3d: the row-boundary warp strips (j0 values)
 };
 
 __device__ __forceinline__ uint32_t vmin2(uint32_t a, uint32_t b) { return __vminu2(a, b); }

@@ -42,8 +42,21 @@
 
 namespace ft {
 
-// bit 15 / 31 of x as 0 / 1 in each 16-bit half
-__device__ __forceinline__ uint32_t hbit(uint32_t x) { return (x >> 15) & 0x10001u; }
+// shared-space address of the dynamic shared memory block of a non-cluster
+// launch (after the 1 KB the hardware reserves); launch_lines3d verifies it
+constexpr uint32_t LINES_SBASE = 0x400;
+constexpr uint32_t LINES_SB2 = LINES_SBASE * 0x10001u;
+
+// bit 15 / 31 of x as 0 / 255 in each 16-bit half: ONE PRMT (sign-replicate
+// byte 1 / byte 3 into byte 0 / byte 2, zero bytes 1 / 3) instead of a shift
+// and a mask -- the signature counts run in units of 255 (row stride 255 K).
+__device__ __forceinline__ uint32_t hff(uint32_t x)
+{
+    uint32_t m;
+    asm("prmt.b32 %0, %1, 0, 0x4B49;" : "=r"(m) : "r"(x));
+    return m;
+}
+constexpr uint32_t FF2 = 0x00FF00FFu;  // 255 in both halves
 // bits 15 / 31 = [prev <= cur] per 16-bit half (levels < 2^15)
 __device__ __forceinline__ uint32_t cmp2(uint32_t prev, uint32_t cur) { return cur + 0x80008000u - prev; }
 
@@ -59,9 +72,13 @@ __device__ __forceinline__ uint32_t pack_pow2_sat(const typename Pair<DT>::T& v,
 {
     const float a = __saturatef((float)v.x * inv);
     const float b = __saturatef((float)v.y * inv);
-    const uint32_t la = __float_as_uint(__fadd_rd(__fmaf_rd(a, Mf, 0.5f), 8388608.0f));
-    const uint32_t lb = __float_as_uint(__fadd_rd(__fmaf_rd(b, Mf, 0.5f), 8388608.0f));
-    return __byte_perm(la, lb, 0x5410) * 4u;
+    // both cells at once: FFMA2.RM then FADD2.RM (packed f32x2, sm_100)
+    const unsigned long long ab = ((unsigned long long)__float_as_uint(b) << 32) | __float_as_uint(a);
+    const unsigned long long m2 = ((unsigned long long)__float_as_uint(Mf) << 32) | __float_as_uint(Mf);
+    unsigned long long y, z;
+    asm("fma.rm.f32x2 %0, %1, %2, %3;" : "=l"(y) : "l"(ab), "l"(m2), "l"(0x3F0000003F000000ull));
+    asm("add.rm.f32x2 %0, %1, %2;" : "=l"(z) : "l"(y), "l"(0x4B0000004B000000ull));
+    return __byte_perm((uint32_t)z, (uint32_t)(z >> 32), 0x5410) * 4u + LINES_SB2;
 }
 
 // Shared-memory increments of both 16-bit halves of a packed address.  No
@@ -69,12 +86,16 @@ __device__ __forceinline__ uint32_t pack_pow2_sat(const typename Pair<DT>::T& v,
 // without an event points at a DUMMY word instead (all such lanes hit the
 // same word: one bank access, merged by the POPC increment).  The halves are
 // split on the FMA pipe (IMAD.HI / IMAD), the ALU pipe being the busy one.
-__device__ __forceinline__ void sinc2(uint32_t sbase, uint32_t addr)
+// Packed level words carry the shared address of the block (LINES_SBASE, in
+// every half), so a half IS the shared address of a signature bin and the
+// plus/minus rows are an immediate above it: ATOMS [R + imm], no base add.
+template <int OFF>
+__device__ __forceinline__ void sinc2(uint32_t addr)
 {
     const uint32_t hi = __umulhi(addr, 0x10000u);
     const uint32_t lo = addr - hi * 0x10000u;
-    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(sbase + lo));
-    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(sbase + hi));
+    asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(lo), "n"(OFF));
+    asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(hi), "n"(OFF));
 }
 // halves of addr whose flag bit (15 / 31) is set, dummy2's halves elsewhere
 __device__ __forceinline__ uint32_t ev_sel(uint32_t flags, uint32_t addr, uint32_t dummy2)
@@ -86,109 +107,125 @@ __device__ __forceinline__ uint32_t ev_sel(uint32_t flags, uint32_t addr, uint32
     return (addr & m) | (dummy2 & ~m);
 }
 
-constexpr int LINES_NTH = 256;          // 8 warp strips per CTA item
-#ifndef LINES_R_DEF
-#define LINES_R_DEF 6
+#ifndef LINES_NTH_DEF
+#define LINES_NTH_DEF 512
 #endif
-#ifndef LINES_PD_DEF
-#define LINES_PD_DEF 2
+#ifndef LINES_MINB_DEF
+#define LINES_MINB_DEF 1
+#endif
+constexpr int LINES_NTH = LINES_NTH_DEF;    // warp strips per CTA item = LINES_NTH / 32
+constexpr int LINES_MINB = LINES_MINB_DEF;  // CTAs per SM the registers are budgeted for
+#ifndef LINES_R_DEF
+#define LINES_R_DEF 4
 #endif
 constexpr int LINES_R = LINES_R_DEF;    // lattice rows per warp strip
-constexpr int LINES_PD = LINES_PD_DEF;  // planes in flight per lane (register ring)
 constexpr int LINES_MINUS = 32768;      // byte offset of the minus row (bit 15 of a packed address)
 
 __host__ __device__ inline int lines_nsig(bool fold) { return fold ? 21 : 7; }
-__host__ __device__ inline int lines_sig_base(int hs, bool fold)
-{
-    return (lines_nsig(fold) + 1) * hs <= LINES_MINUS ? hs : LINES_MINUS + hs;
-}
-__host__ __device__ inline int lines_end(int hs, bool fold)
-{
-    const int a = LINES_MINUS + hs, b = lines_sig_base(hs, fold) + lines_nsig(fold) * hs;
-    return a > b ? a : b;
-}
+// Shared layout: signature rows at 0 (at most 64 KB: the 16-bit packed row
+// offsets), the plus row at LINES_PLUS and the minus row LINES_MINUS above
+// it; both bases are constants, so every ATOMS address is [R + UR (+imm)].
+constexpr int LINES_PLUS = 65536;
+__host__ __device__ inline int lines_end(int hs, bool) { return LINES_PLUS + LINES_MINUS + hs; }
 
 // One warp strip (R lattice rows x 60 lattice columns) marching the planes of
-// a chunk [ia, ib).  Shared memory: plus row at 0, minus row at LINES_MINUS
-// (EC events of the B/C/D lines, and of the A lines unless FOLD), signature
-// rows at sig_base.
-template <int DT, int QM, bool VEC, int R, bool FOLD, bool GUARD>
+// a chunk [ia, ib).  Shared memory (lines_end): signature rows at 0, the
+// plus / minus rows of the EC events of the B/C/D lines (and of the A lines
+// unless FOLD) at LINES_PLUS / LINES_PLUS + LINES_MINUS.
+template <int DT, int QM, bool VEC, int R, bool FOLD, int DS, bool ROWFIX>
 __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restrict__ buf, const LGeo& g,
                                            const QuantDev& q, const float* __restrict__ tt, char* __restrict__ h,
-                                           int sig_base, int64_t ia, int64_t ib, int j0, int k0, int lane)
+                                           int64_t ia, int64_t ib, int j0, int k0, int lane)
 {
     using P2 = typename Pair<DT>::T;
     using T = typename Elem<DT>::T;
     constexpr int NR = R + 2;  // cell rows j0-1 .. j0+R held per plane
     constexpr uint32_t FULL = 0xFFFFFFFFu;
-    const int Di = (int)g.D;
-    const int64_t pe = g.W * g.D;
+    // DS > 0: the row stride D as a compile-time constant, so the NR row loads
+    // of a plane use immediate offsets from one pointer (no address math)
+    const int Di = DS > 0 ? DS : (int)g.D;
+    const int64_t pe = g.W * (int64_t)Di;
     const uint32_t sent4 = (uint32_t)(g.M + 1) * 4u;
-    const uint32_t hs = (uint32_t)g.hs;
+    const uint32_t S2 = sent4 * 0x10001u + LINES_SB2;  // sentinel level word (with the shared base)
+    const uint32_t hk = (uint32_t)g.hk;  // signature row stride / 255
     const float Mf = (float)g.M;
     const int kk = k0 - 2 + 2 * lane;
     const bool computes = lane >= 1 && lane <= 30;
-    const uint32_t lmask = computes ? FULL : 0u;  // halo lanes 0 / 31 book nothing
-    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(h);
-    const uint32_t ssig = sb + (uint32_t)sig_base;
-    const uint32_t dummy2 = sent4 * 0x10001u;   // sentinel bin of the plus row (never read)
+    // halo lanes 0 / 31 book nothing; through a shuffle so that ptxas keeps a
+    // mask register (one 3-input LOP3) instead of SEL on a predicate
+    const uint32_t lmask = __shfl_sync(FULL, computes ? FULL : 0u, lane);
+    const uint32_t dummy2 = S2;    // sentinel bin (never read) of signature row 0 / the plus row
     const int n = (int)(ib - ia);
 
-    // planes t = -1 .. n (plane ia-1+t) exist iff t_lo <= t < t_hi (warp-uniform;
-    // only the first two and the last plane of the field can be absent)
+    // Absent cells (outside the field) read as the sentinel:
+    // * planes t = -1 .. n (plane ia-1+t) exist iff t_lo <= t < t_hi (warp-
+    //   uniform; only the first two and the last plane of the field);
+    // * columns: each lane loads a CLAMPED in-row pair (always valid memory)
+    //   and masks absent cells per 16-bit half (lanekeep, one LOP3 per row);
+    // * rows: warp strips at the j boundary (rowfix, warp-uniform) predicate
+    //   their row loads and overwrite absent rows.
     const int t_lo = (int)max((int64_t)-1, 1 - ia);
     const int t_hi = (int)min((int64_t)(n + 2), g.H - ia + 1);
-    bool okx = true, oky = true;
-    uint32_t rowok = FULL;
-    if constexpr (GUARD) {
-        okx = kk >= 0 && kk < Di;
-        oky = kk >= 0 && kk + 1 < Di;
+    const bool okx = kk >= 0 && kk < (int)g.D, oky = kk + 1 >= 0 && kk + 1 < (int)g.D;
+    const uint32_t lanekeep = (okx ? 0x0000FFFFu : 0u) | (oky ? 0xFFFF0000u : 0u);
+    const int kc = VEC ? min(max(kk, 0), (int)g.D - 2) : min(max(kk, 0), (int)g.D - 1);
+    uint32_t rowok = (1u << NR) - 1u;
+    if constexpr (ROWFIX) {
         rowok = 0;
 #pragma unroll
         for (int r = 0; r < NR; ++r) rowok |= (j0 - 1 + r >= 0 && j0 - 1 + r < (int)g.W) ? 1u << r : 0u;
     }
-    const uint32_t lanekeep = (okx ? 0x0000FFFFu : 0u) | (oky ? 0xFFFF0000u : 0u);
     // word of row 0 in plane ia-2 (t = -1)
-    const T* ptr = buf + ((ia - 2 - g.first) * pe + (int64_t)(j0 - 1) * Di + (okx ? kk : 0));
+    const T* ptr = buf + ((ia - 2 - g.first) * pe + (int64_t)(j0 - 1) * Di + kc);
 
     auto fetch = [&](int t, const T* at, P2(&dst)[NR]) {
-        const bool pin = t >= t_lo && t < t_hi;
-        if constexpr (GUARD) {
+        if (t >= t_lo && t < t_hi) {
+            if constexpr (ROWFIX) {
 #pragma unroll
-            for (int r = 0; r < NR; ++r) {
-                const bool ok = pin && ((rowok >> r) & 1u);
-                dst[r] = load_pair<DT, VEC>(at + r * Di, ok && okx, ok && oky);
-            }
-        } else {
-            if (pin) {
+                for (int r = 0; r < NR; ++r)
+                    if ((rowok >> r) & 1u) dst[r] = load_pair<DT, VEC>(at + r * Di, true, kk + 1 < (int)g.D);
+            } else {
 #pragma unroll
-                for (int r = 0; r < NR; ++r) dst[r] = load_pair<DT, VEC>(at + r * Di, true, true);
+                for (int r = 0; r < NR; ++r) dst[r] = load_pair<DT, VEC>(at + r * Di, true, kk + 1 < (int)g.D);
             }
         }
     };
+    // quantize a plane known to exist
+    auto quant_in = [&](const P2(&src)[NR], uint32_t(&V)[NR]) {
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+            uint32_t v;
+            if constexpr (QM == FT_Q_POW2)
+                v = pack_pow2_sat<DT>(src[r], q.inv, Mf);
+            else
+                v = pack_pair<DT, QM, 0>(src[r], true, true, tt, q, g.M, sent4) + LINES_SB2;
+            V[r] = (v & lanekeep) | (S2 & ~lanekeep);
+        }
+        if constexpr (ROWFIX) {
+#pragma unroll
+            for (int r = 0; r < NR; ++r)
+                if (!((rowok >> r) & 1u)) V[r] = S2;
+        }
+    };
     auto quant = [&](int t, const P2(&src)[NR], uint32_t(&V)[NR]) {
-        const bool pin = t >= t_lo && t < t_hi;
-        if constexpr (GUARD) {
+        if (t >= t_lo && t < t_hi) {
 #pragma unroll
             for (int r = 0; r < NR; ++r) {
-                const bool ok = pin && ((rowok >> r) & 1u);
+                uint32_t v;
                 if constexpr (QM == FT_Q_POW2)
-                    V[r] = pack_pair_pow2<DT>(src[r], ok ? lanekeep : 0u, q.scale, (uint32_t)g.M * 0x10001u,
-                                              sent4 * 0x10001u);
+                    v = pack_pow2_sat<DT>(src[r], q.inv, Mf);
                 else
-                    V[r] = pack_pair<DT, QM, 0>(src[r], ok && okx, ok && oky, tt, q, g.M, sent4);
+                    v = pack_pair<DT, QM, 0>(src[r], true, true, tt, q, g.M, sent4) + LINES_SB2;
+                V[r] = (v & lanekeep) | (S2 & ~lanekeep);
             }
-        } else if (pin) {
+            if constexpr (ROWFIX) {
 #pragma unroll
-            for (int r = 0; r < NR; ++r) {
-                if constexpr (QM == FT_Q_POW2)
-                    V[r] = pack_pow2_sat<DT>(src[r], q.inv, Mf);
-                else
-                    V[r] = pack_pair<DT, QM, 0>(src[r], true, true, tt, q, g.M, sent4);
+                for (int r = 0; r < NR; ++r)
+                    if (!((rowok >> r) & 1u)) V[r] = S2;
             }
         } else {
 #pragma unroll
-            for (int r = 0; r < NR; ++r) V[r] = sent4 * 0x10001u;
+            for (int r = 0; r < NR; ++r) V[r] = S2;
         }
     };
     // k-shifted words and the min-derived families of one plane
@@ -200,157 +237,184 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
         }
     };
 
-    uint32_t pV[NR], tmi[R + 1], pWm[R + 1], pWp[R + 1];
-    uint32_t pB[R + 1], eB[R + 1], pC[R + 1], eC[R + 1], pD[R + 1], eD[R + 1];
-    P2 rbuf[LINES_PD][NR];  // planes in flight per lane
+    // march state of the previous cell plane; two copies, written alternately
+    // by the 2-step unrolled march, so no register moves carry it over
+    struct St {
+        uint32_t pV[NR], tmi[R + 1], pWm[R + 1];
+        uint32_t pB[R + 1], eB[R + 1], pC[R + 1], eC[R + 1], pD[R + 1], eD[R + 1];
+    };
+    St sa, sb2;
+    P2 ra[NR], rb[NR];  // two planes in flight per lane
     {
-        fetch(-1, ptr, rbuf[0]);
-        fetch(0, ptr + pe, rbuf[1]);
+        fetch(-1, ptr, ra);
+        fetch(0, ptr + pe, rb);
         uint32_t V0[NR], Wm0[NR], C0[NR], Wm1[NR], C1[NR];
-        quant(-1, rbuf[0], V0);  // plane ia-2
-        quant(0, rbuf[1], pV);   // plane ia-1
+        quant(-1, ra, V0);       // plane ia-2
+        quant(0, rb, sa.pV);     // plane ia-1
         derive(V0, Wm0, C0);
-        derive(pV, Wm1, C1);
+        derive(sa.pV, Wm1, C1);
 #pragma unroll
         for (int r = 1; r <= R; ++r) {
-            tmi[r] = hbit(cmp2(V0[r], pV[r]));
-            pWm[r] = Wm1[r];
-            pWp[r] = shift_pair(pV[r], __shfl_down_sync(FULL, pV[r], 1));
-            const uint32_t b0 = vmin2(V0[r - 1], V0[r]), b1 = vmin2(pV[r - 1], pV[r]);
+            sa.tmi[r] = hff(cmp2(V0[r], sa.pV[r]));
+            sa.pWm[r] = Wm1[r];
+            const uint32_t b0 = vmin2(V0[r - 1], V0[r]), b1 = vmin2(sa.pV[r - 1], sa.pV[r]);
             const uint32_t d0 = vmin2(C0[r - 1], C0[r]), d1 = vmin2(C1[r - 1], C1[r]);
-            pB[r] = b1;
-            eB[r] = cmp2(b0, b1);
-            pC[r] = C1[r];
-            eC[r] = cmp2(C0[r], C1[r]);
-            pD[r] = d1;
-            eD[r] = cmp2(d0, d1);
+            sa.pB[r] = b1;
+            sa.eB[r] = cmp2(b0, b1);
+            sa.pC[r] = C1[r];
+            sa.eC[r] = cmp2(C0[r], C1[r]);
+            sa.pD[r] = d1;
+            sa.eD[r] = cmp2(d0, d1);
         }
     }
-#pragma unroll
-    for (int u = 0; u < LINES_PD; ++u) fetch(1 + u, ptr + (2 + u) * pe, rbuf[u]);
-    ptr += (2 + LINES_PD) * pe;  // next fetch: t = 1 + LINES_PD
+    fetch(1, ptr + 2 * pe, ra);
+    fetch(2, ptr + 3 * pe, rb);
+    ptr += 4 * pe;  // next fetch: t = 3
 
     // One step: plane t (cell plane p = ia-1+t) arrives in V; every event of
-    // cell plane p-1 (whose +i neighbours are now known) is booked.
-    auto step = [&](const uint32_t(&V)[NR]) {
+    // cell plane p-1 (whose +i neighbours are now known) is booked.  o = the
+    // state of plane p-1, x receives the state of plane p.
+    auto step = [&](const uint32_t(&V)[NR], const St& o, St& x) {
         uint32_t Wm[NR], C[NR];
         derive(V, Wm, C);
         uint32_t tpj = 0;
 #pragma unroll
         for (int r = 1; r <= R; ++r) {
             const uint32_t W_ = V[r];
-            const uint32_t Wp = shift_pair(W_, __shfl_down_sync(FULL, W_, 1));
             // signature of the plane-(p-1) cell: "face neighbour n activates
             // first" = bit 15 / 31 of c' - n + k (k = 0 for -side, -1 for +side)
-            const uint32_t cb = pV[r] | 0x80008000u;
-            const uint32_t t1 = r == 1 ? hbit(cb - pV[0]) : 0x10001u - tpj;  // -j
-            const uint32_t t2 = hbit(cb - pWm[r]);                            // -k
-            const uint32_t t3 = hbit(cb - W_ - 0x10001u);                     // +i
-            const uint32_t t4 = hbit(cb - pV[r + 1] - 0x10001u);              // +j
-            const uint32_t t5 = hbit(cb - pWp[r] - 0x10001u);                 // +k
+            const uint32_t cb = o.pV[r] | 0x80008000u;
+            const uint32_t t1 = r == 1 ? hff(cb - o.pV[0]) : FF2 - tpj;  // -j
+            const uint32_t t2 = hff(cb - o.pWm[r]);                      // -k
+            const uint32_t t3 = hff(cb - W_ - 0x10001u);                 // +i
+            const uint32_t t4 = hff(cb - o.pV[r + 1] - 0x10001u);        // +j
+            // +k: "right neighbour first" is the complement of the right
+            // neighbour's -k term (lo: this word's hi half, hi: the next lane's lo)
+            const uint32_t t5 = FF2 - shift_pair(t2, __shfl_down_sync(FULL, t2, 1));
             uint32_t evS;
             if constexpr (FOLD) {
-                // row u + 7 (s_i + 1) = (t1 + t2 + t4 + t5) + 14 - 6 (tmi + t3); no
-                // half borrows: 14 - 6 n_i >= 2
-                const uint32_t row = (tmi[r] + t3) * (uint32_t)(-6) + (t1 + t2 + t4 + t5 + 0x000E000Eu);
-                evS = row * hs + pV[r];
+                // row u + 7 (s_i + 1) = (t1 + t2 + t4 + t5) + 14 - 6 (tmi + t3), in
+                // units of 255; no half borrows: 14 - 6 n_i >= 2
+                const uint32_t row = (o.tmi[r] + t3) * (uint32_t)(-6) + (t1 + t2 + t4 + t5 + 14u * FF2);
+                evS = row * hk + o.pV[r];
             } else {
-                evS = (tmi[r] + t1 + t2 + t3 + t4 + t5) * hs + pV[r];
+                evS = (o.tmi[r] + t1 + t2 + t3 + t4 + t5) * hk + o.pV[r];
                 // A line event iff both or neither i-neighbour is first; minus (max) iff t3
-                const uint32_t fA = ~(tmi[r] ^ t3) & (lmask & 0x00010001u);
-                const uint32_t aA = pV[r] | (t3 << 15);
-                sinc2(sb, ev_sel(fA << 15, aA, dummy2));
+                const uint32_t fA = ~(o.tmi[r] ^ t3) & lmask;
+                const uint32_t aA = o.pV[r] | ((t3 << 8) & 0x80008000u);
+                sinc2<LINES_PLUS>(ev_sel(fA << 8, aA, dummy2));
             }
-            sinc2(ssig, (evS & lmask) | (dummy2 & ~lmask));  // halo lanes: sentinel bin of row 0
+            sinc2<0>((evS & lmask) | (dummy2 & ~lmask));  // halo lanes: sentinel bin of row 0
             // B / C / D lines: event iff the along-i order flips at p-1; sign -1
             // (B, C): local min -> minus row; sign +1 (D): local max -> minus row
             const uint32_t B = vmin2(V[r - 1], W_);
             const uint32_t D = vmin2(C[r - 1], C[r]);
-            const uint32_t nB = cmp2(pB[r], B), nC = cmp2(pC[r], C[r]), nD = cmp2(pD[r], D);
-            sinc2(sb, ev_sel((eB[r] ^ nB) & lmask, pB[r] | (nB & 0x80008000u), dummy2));
-            sinc2(sb, ev_sel((eC[r] ^ nC) & lmask, pC[r] | (nC & 0x80008000u), dummy2));
-            sinc2(sb, ev_sel((eD[r] ^ nD) & lmask, pD[r] | (~nD & 0x80008000u), dummy2));
-            tmi[r] = 0x10001u - t3;
+            const uint32_t nB = cmp2(o.pB[r], B), nC = cmp2(o.pC[r], C[r]), nD = cmp2(o.pD[r], D);
+            sinc2<LINES_PLUS>(ev_sel((o.eB[r] ^ nB) & lmask, o.pB[r] | (nB & 0x80008000u), dummy2));
+            sinc2<LINES_PLUS>(ev_sel((o.eC[r] ^ nC) & lmask, o.pC[r] | (nC & 0x80008000u), dummy2));
+            sinc2<LINES_PLUS>(ev_sel((o.eD[r] ^ nD) & lmask, o.pD[r] | (~nD & 0x80008000u), dummy2));
+            x.tmi[r] = FF2 - t3;
             tpj = t4;
-            pWm[r] = Wm[r];
-            pWp[r] = Wp;
-            pB[r] = B;
-            eB[r] = nB;
-            pC[r] = C[r];
-            eC[r] = nC;
-            pD[r] = D;
-            eD[r] = nD;
+            x.pWm[r] = Wm[r];
+            x.pB[r] = B;
+            x.eB[r] = nB;
+            x.pC[r] = C[r];
+            x.eC[r] = nC;
+            x.pD[r] = D;
+            x.eD[r] = nD;
         }
 #pragma unroll
-        for (int r = 0; r < NR; ++r) pV[r] = V[r];
+        for (int r = 0; r < NR; ++r) x.pV[r] = V[r];
     };
 
-    // rbuf[u] holds plane t = s + 1 + u at the top of each unrolled round
+    // steps s < nm see an existing plane t = s+1; only the last step of the
+    // field's last chunk (plane H) can follow, with a sentinel plane
     uint32_t V[NR];
-    for (int s = 0; s < n; s += LINES_PD) {
-#pragma unroll
-        for (int u = 0; u < LINES_PD; ++u) {
-            if (s + u < n) {
-                quant(s + u + 1, rbuf[u], V);
-                if (s + u + LINES_PD < n) fetch(s + u + 1 + LINES_PD, ptr, rbuf[u]);
-                ptr += pe;
-                step(V);
-            }
+    const int nm = min(n, t_hi - 1);
+    const int tf = min(n + 1, t_hi);  // planes t < tf are fetched
+    int s = 0;
+    for (; s < nm; s += 2) {
+        quant_in(ra, V);  // plane t = s+1
+        if (s + 3 < tf) fetch(s + 3, ptr, ra);
+        ptr += pe;
+        step(V, sa, sb2);
+        if (s + 1 >= nm) {
+            ++s;
+            break;
         }
+        quant_in(rb, V);
+        if (s + 4 < tf) fetch(s + 4, ptr, rb);
+        ptr += pe;
+        step(V, sb2, sa);
+    }
+    if (s < n) {  // at most one step: the absent plane H
+#pragma unroll
+        for (int r = 0; r < NR; ++r) V[r] = S2;
+        if (s & 1)
+            step(V, sb2, sa);
+        else
+            step(V, sa, sb2);
     }
 }
 
-// GUARD = false: the interior tiles [ti_j0, ti_j1) x [ti_k0, ti_k1), every
-// warp strip of which has all its rows and columns inside the field (no load
-// predicates, no sentinel selects); GUARD = true: every other tile.  Two
-// kernels rather than one branch, so that the boundary code's register
-// pressure cannot spill in the interior loop.
-template <int DT, int QM, bool VEC, int R, bool FOLD, bool GUARD>
-__global__ void __launch_bounds__(LINES_NTH, 2) lines3d_kernel(const typename Elem<DT>::T* __restrict__ buf, LGeo g,
-                                                               QuantDev q, unsigned long long* __restrict__ hist)
+// ROWFIX = false: every warp strip whose rows j0-1 .. j0+R all lie in the
+// field (columns and planes are masked in-line); ROWFIX = true: the few strips
+// at the j boundary, with row-predicated loads.  Two launches rather than a
+// branch, so that the boundary code cannot cost the main loop registers.
+template <int DT, int QM, bool VEC, int R, bool FOLD, int DS, bool ROWFIX>
+__global__ void __launch_bounds__(LINES_NTH, LINES_MINB) lines3d_kernel(const typename Elem<DT>::T* __restrict__ buf,
+                                                                        LGeo g, QuantDev q,
+                                                                        unsigned long long* __restrict__ hist)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     char* h = reinterpret_cast<char*>(smem_raw);
     const int M2 = g.M + 2;
     const int hs = g.hs;
-    const int sig_base = lines_sig_base(hs, FOLD);
     const int end = lines_end(hs, FOLD);
-    float* tt = reinterpret_cast<float*>(h + end);
+    float* tt = reinterpret_cast<float*>(h + LINES_PLUS + hs);  // threshold table: in the plus/minus gap
     for (int i = threadIdx.x; i < end / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(h)[i] = 0;
+    __syncthreads();  // the table lies inside the zeroed range
     if (QM != FT_Q_IDENTITY && QM != FT_Q_POW2)
         for (int i = threadIdx.x; i < M2; i += blockDim.x) tt[i] = q.tt[i];
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x / 32;
-    const int nj = g.ti_j1 - g.ti_j0, nk = g.ti_k1 - g.ti_k0;
-    const int64_t per_chunk = GUARD ? (int64_t)g.tiles_j * g.tiles_k : (int64_t)nj * nk;
-    for (int64_t item = blockIdx.x; item < g.n_items; item += gridDim.x) {
-        const int64_t ch = item / per_chunk;
-        const int rem = (int)(item - ch * per_chunk);
-        int tj, tk;
-        if constexpr (GUARD) {
-            tj = rem / g.tiles_k;
-            tk = rem % g.tiles_k;
-            if (tj >= g.ti_j0 && tj < g.ti_j1 && tk >= g.ti_k0 && tk < g.ti_k1) continue;  // the other kernel's
-        } else {
-            tj = g.ti_j0 + rem / nk;
-            tk = g.ti_k0 + rem % nk;
+    if constexpr (ROWFIX) {
+        // one warp per (chunk, column tile, row-boundary strip): these strips are
+        // few, so they are spread over all warps of the grid
+        const int64_t nw = (int64_t)gridDim.x * (LINES_NTH / 32);
+        const int64_t per_chunk = (int64_t)g.tiles_k * g.rf_n;
+        for (int64_t it = (int64_t)blockIdx.x * (LINES_NTH / 32) + warp; it < g.n_items; it += nw) {
+            const int64_t ch = it / per_chunk;
+            const int rem = (int)(it - ch * per_chunk);
+            const int j0 = g.rf_j0[rem % g.rf_n];
+            const int k0 = (rem / g.rf_n) * 60;
+            const int64_t ia = g.v0 + ch * g.chunk;
+            const int64_t ib = min(ia + (int64_t)g.chunk, g.v1);
+            lines_item<DT, QM, VEC, R, FOLD, DS, true>(buf, g, q, tt, h, ia, ib, j0, k0, lane);
         }
-        const int j0 = tj * (8 * R) + warp * R;
-        const int k0 = tk * 60;
-        const int64_t ia = g.v0 + ch * g.chunk;
-        const int64_t ib = min(ia + (int64_t)g.chunk, g.v1);
-        lines_item<DT, QM, VEC, R, FOLD, GUARD>(buf, g, q, tt, h, sig_base, ia, ib, j0, k0, lane);
+    } else {
+        const int64_t per_chunk = (int64_t)g.tiles_j * g.tiles_k;
+        for (int64_t item = blockIdx.x; item < g.n_items; item += gridDim.x) {
+            const int64_t ch = item / per_chunk;
+            const int rem = (int)(item - ch * per_chunk);
+            const int j0 = (rem / g.tiles_k) * ((LINES_NTH / 32) * R) + warp * R;
+            const int k0 = (rem % g.tiles_k) * 60;
+            if (!(j0 >= 1 && j0 + R < g.W)) continue;  // past the lattice or a row-boundary strip
+            const int64_t ia = g.v0 + ch * g.chunk;
+            const int64_t ib = min(ia + (int64_t)g.chunk, g.v1);
+            lines_item<DT, QM, VEC, R, FOLD, DS, false>(buf, g, q, tt, h, ia, ib, j0, k0, lane);
+        }
     }
     __syncthreads();
     // fold: C = sum of signature rows, F = sum (6 - u) rows, EC = A events (row
     // groups, or plus/minus when !FOLD) + plus - minus, X = EC - F + C
     const uint32_t* hw = reinterpret_cast<const uint32_t*>(h);
-    const int rw = hs / 4, sb = sig_base / 4;
+    const int rw = hs / 4, sb = 0, pm = LINES_PLUS / 4;
     for (int l = threadIdx.x; l < M2; l += blockDim.x) {
         uint32_t c = 0, f = 0;
-        int32_t ec = (int32_t)(hw[l] - hw[LINES_MINUS / 4 + l]);
+        int32_t ec = (int32_t)(hw[pm + l] - hw[pm + LINES_MINUS / 4 + l]);
 #pragma unroll
         for (int s = 0; s < lines_nsig(FOLD); ++s) {
             const uint32_t v = hw[sb + s * rw + l];
@@ -366,42 +430,106 @@ __global__ void __launch_bounds__(LINES_NTH, 2) lines3d_kernel(const typename El
 }
 
 // 16-bit packed signature offsets: (rows - 1) * hs + level * 4 must fit
-static bool lines_fold_ok(int M, int hs) { return 20 * hs + (M + 1) * 4 <= 0xFFFF; }
+// signature rows are 255 K bytes apart (K a multiple of 4: word-aligned rows)
+static int lines_hs(int M) { return 255 * (int)cdiv(cdiv((int64_t)(M + 2) * 4, 255), 4) * 4; }
+// 16-bit packed signature offsets: (rows - 1) * hs + level * 4 must fit
+static bool lines_fold_ok(int M, int hs)
+{
+    return 20 * hs + (M + 1) * 4 + (int)LINES_SBASE < LINES_PLUS && (M + 2) * 4 <= hs;
+}
 static bool lines_ok(int M)
 {
-    const int hs = ((M + 2) * 4 + 15) / 16 * 16;
-    return (M + 1) * 4 < LINES_MINUS && 6 * hs + (M + 1) * 4 <= 0xFFFF;
+    return (M + 1) * 4 + (int)LINES_SBASE < LINES_MINUS && 6 * lines_hs(M) + (M + 1) * 4 + (int)LINES_SBASE < LINES_PLUS &&
+           lines_hs(M) + (M + 2) * 4 <= LINES_MINUS;
 }
 
-template <int DT, int QM, bool VEC, bool FOLD, bool GUARD>
-static int launch_lines_kernel(const ft_window* win, LGeo g, const QuantDev& qd, size_t smem, int64_t items_per_chunk,
-                               int64_t nchunks, uint64_t* hist, cudaStream_t st)
+__global__ void lines_sbase_probe(uint32_t* out)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    *out = (uint32_t)__cvta_generic_to_shared(smem_raw);
+}
+
+// The kernels address shared memory absolutely (LINES_SBASE): check once.
+static int lines_check_sbase()
+{
+    static int state = -1;  // -1 unchecked, FT_OK, or an error code
+    if (state >= 0) return state;
+    uint32_t *d = nullptr, v = 0;
+    if (cudaMalloc(&d, 4) != cudaSuccess) return FT_ERR_CUDA_BASE + (int)cudaGetLastError();
+    lines_sbase_probe<<<1, 1, 16>>>(d);
+    const cudaError_t e = cudaMemcpy(&v, d, 4, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return FT_ERR_CUDA_BASE + (int)e;
+    state = v == LINES_SBASE ? FT_OK : FT_ERR_CLASSIFY;
+    return state;
+}
+
+// Plane chunks: about 16 items per CTA (the warps of a CTA march
+// independently, so the kernel lasts as long as its busiest warp's strips),
+// marches of >= 64 planes.
+static int lines_chunk(int64_t rows, int64_t tiles, int64_t ctas)
+{
+    const int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>(cdiv(16 * ctas, std::max<int64_t>(tiles, 1)),
+                                                                   rows / 64));
+    return (int)cdiv(rows, nchunks);
+}
+
+template <int DT, int QM, bool VEC, bool FOLD, int DS, bool ROWFIX>
+static int launch_lines_kernel(const ft_window* win, LGeo g, const QuantDev& qd, size_t smem, uint64_t* hist,
+                               cudaStream_t st)
 {
     using T = typename Elem<DT>::T;
-    if (items_per_chunk <= 0) return FT_OK;
-    auto kern = lines3d_kernel<DT, QM, VEC, LINES_R, FOLD, GUARD>;
+    auto kern = lines3d_kernel<DT, QM, VEC, LINES_R, FOLD, DS, ROWFIX>;
     FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     FT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, LINES_NTH, smem));
     if (per_sm < 1) return FT_ERR_ARG;
-    g.n_items = (GUARD ? (int64_t)g.tiles_j * g.tiles_k : items_per_chunk) * nchunks;
-    const int64_t grid = std::min<int64_t>((int64_t)nsm_l() * per_sm, GUARD ? items_per_chunk * nchunks : g.n_items);
+    const int64_t cap = (int64_t)nsm_l() * per_sm;
+    int64_t grid;
+    if (ROWFIX) {
+        // row-boundary strips: j0 = 0 and every strip reaching row W-1 or past it
+        g.rf_n = 0;
+        for (int64_t j0 = 0; j0 <= g.W && g.rf_n < 4; j0 += LINES_R)
+            if (j0 < 1 || j0 + LINES_R >= g.W) g.rf_j0[g.rf_n++] = (int)j0;
+        if (g.rf_n == 0) return FT_OK;
+        if (g.rf_n == 4 && g.W > 3 * LINES_R) return FT_ERR_ARG;  // unreachable: at most 3 strips
+        // one warp per strip-chunk: chunks short enough to fill the grid's warps
+        const int64_t strips = (int64_t)g.tiles_k * g.rf_n;
+        g.chunk = lines_chunk(g.v1 - g.v0, cdiv(strips, LINES_NTH / 32), cap);
+        g.n_items = strips * cdiv(g.v1 - g.v0, g.chunk);
+        grid = std::min<int64_t>(cap, cdiv(g.n_items, LINES_NTH / 32));
+    } else {
+        const int64_t tiles = (int64_t)g.tiles_j * g.tiles_k;
+        g.chunk = lines_chunk(g.v1 - g.v0, tiles, cap);
+        g.n_items = tiles * cdiv(g.v1 - g.v0, g.chunk);
+        grid = std::min<int64_t>(cap, g.n_items);
+    }
     kern<<<(int)grid, LINES_NTH, smem, st>>>(static_cast<const T*>(win->data), g, qd,
                                             reinterpret_cast<unsigned long long*>(hist));
     FT_CUDA_TRY(cudaGetLastError());
     return FT_OK;
 }
 
+template <int DT, int QM, bool VEC, bool FOLD, int DS>
+static int launch_lines_two(const ft_window* win, const LGeo& g, const QuantDev& qd, size_t smem, uint64_t* hist,
+                            cudaStream_t st)
+{
+    const int rc = launch_lines_kernel<DT, QM, VEC, FOLD, DS, false>(win, g, qd, smem, hist, st);
+    return rc ? rc : launch_lines_kernel<DT, QM, VEC, FOLD, DS, true>(win, g, qd, smem, hist, st);
+}
+
 template <int DT, int QM, bool VEC, bool FOLD>
 static int launch_lines_pair(const ft_window* win, const LGeo& g, const QuantDev& qd, size_t smem, uint64_t* hist,
                              cudaStream_t st)
 {
-    const int64_t nchunks = cdiv(g.v1 - g.v0, g.chunk);
-    const int64_t inner = (int64_t)(g.ti_j1 - g.ti_j0) * (g.ti_k1 - g.ti_k0);
-    const int64_t outer = (int64_t)g.tiles_j * g.tiles_k - inner;
-    int rc = launch_lines_kernel<DT, QM, VEC, FOLD, false>(win, g, qd, smem, inner, nchunks, hist, st);
-    if (rc) return rc;
-    return launch_lines_kernel<DT, QM, VEC, FOLD, true>(win, g, qd, smem, outer, nchunks, hist, st);
+    // specialised on the common row lengths (BASELINE configs)
+    switch (VEC ? g.D : 0) {
+    case 2048: return launch_lines_two<DT, QM, VEC, FOLD, 2048>(win, g, qd, smem, hist, st);
+    case 1024: return launch_lines_two<DT, QM, VEC, FOLD, 1024>(win, g, qd, smem, hist, st);
+    case 512: return launch_lines_two<DT, QM, VEC, FOLD, 512>(win, g, qd, smem, hist, st);
+    case 256: return launch_lines_two<DT, QM, VEC, FOLD, 256>(win, g, qd, smem, hist, st);
+    default: return launch_lines_two<DT, QM, VEC, FOLD, 0>(win, g, qd, smem, hist, st);
+    }
 }
 
 template <int DT, int QM>
@@ -412,23 +540,14 @@ static int launch_lines3d(const ft_window* win, int64_t H, int64_t W, int64_t D,
     constexpr int R = LINES_R, TJ = (LINES_NTH / 32) * R;
     LGeo g{};
     g.H = H; g.W = W; g.D = D; g.v0 = v0; g.v1 = v1; g.first = win->first; g.M = M;
-    g.hs = ((M + 2) * 4 + 15) / 16 * 16;
+    g.hs = lines_hs(M);
+    g.hk = g.hs / 255;
     const bool vec = D % 2 == 0 && reinterpret_cast<uintptr_t>(win->data) % (2 * sizeof(T)) == 0;
     const bool fold = lines_fold_ok(M, g.hs);
-    size_t smem = (size_t)lines_end(g.hs, fold);
-    if (QM != FT_Q_IDENTITY && QM != FT_Q_POW2) smem += (size_t)(M + 2) * 4;
+    const size_t smem = (size_t)lines_end(g.hs, fold);
     g.tiles_j = (int)cdiv(W + 1, TJ);
     g.tiles_k = (int)cdiv(D + 1, 60);
-    // interior tiles: every strip's rows j0-1 .. j0+R in [0, W), cells k0-2 .. k0+61 in [0, D)
-    g.ti_j0 = 1;
-    g.ti_j1 = W >= TJ + 1 ? (int)((W - TJ - 1) / TJ) + 1 : 0;
-    g.ti_k0 = 1;
-    g.ti_k1 = D >= 62 ? (int)((D - 62) / 60) + 1 : 0;
-    if (g.ti_j1 <= g.ti_j0 || g.ti_k1 <= g.ti_k0) g.ti_j0 = g.ti_j1 = g.ti_k0 = g.ti_k1 = 0;
-    // plane chunks: enough items to balance ~2 CTAs per SM, marches >= 128 planes
-    const int64_t tiles = (int64_t)g.tiles_j * g.tiles_k, rows = v1 - v0;
-    int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>(cdiv(16 * 2 * nsm_l(), tiles), rows / 128));
-    g.chunk = (int)cdiv(rows, nchunks);
+    if (const int rc = lines_check_sbase()) return rc;
     QuantDev qd = qdev(qa);
     if (QM == FT_Q_POW2) qd.inv = M > 0 ? qd.scale / (float)M : 0.f;
     if (fold)
