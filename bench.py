@@ -42,6 +42,21 @@ CONFIGS = {
 }
 
 
+def ncu_traffic(path=ROOT / "profiles" / "r01" / "ncu_lines3d_main.txt"):
+    """DRAM bytes (read + write) per launch of the main kernel from the committed
+    ncu --set full summary (None when absent)."""
+    try:
+        vals = {}
+        for line in path.read_text().splitlines():
+            parts = line.split()
+            if len(parts) >= 3 and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}[parts[2]]
+                vals[parts[0]] = float(parts[1]) * scale
+        return int(sum(vals.values())) if len(vals) == 2 else None
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -323,7 +338,10 @@ def main():
                "data": "synthetic (seeded device-generated GRF; no dataset in the reference)",
                "config": config,
                "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
-                            "frac": round(achieved / peak, 4), "traffic": None,
+                            "frac": round(achieved / peak, 4),
+                            "traffic": ncu_traffic() if plan[0] == "lines" and (H, W, D) == (2048, 2048, 2048) else None,
+                            "traffic_source": "profiles/r01/ncu_lines3d_main.txt (ncu --set full, main launch, "
+                                              "dram__bytes_read + dram__bytes_write)",
                             "kernel": kname + ", per-launch median over CUDA events",
                             "kernel_ms": round(kms, 4), "peak_source": peak_kind,
                             "algorithmic_bytes_per_launch": int(bytes_per_launch)},
