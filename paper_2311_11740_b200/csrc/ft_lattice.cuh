@@ -24,6 +24,8 @@ struct LGeo {
     int ti_j0, ti_j1, ti_k0, ti_k1;  // ft_lines3d: interior tile ranges (guard-free kernel)
     int hk;                          // ft_lines3d: signature row stride / 255
     int rf_n, rf_j0[4];              // ft_lines3d: the row-boundary warp strips (j0 values)
+    int kb_lo, kb_hi;                // ft_lines3d: k-boundary column tiles at each end
+    uint32_t one, four;              // ft_lines3d: 1 and 4 as opaque registers (IMAD, not IADD3/LEA)
 };
 
 __device__ __forceinline__ uint32_t vmin2(uint32_t a, uint32_t b) { return __vminu2(a, b); }

@@ -68,7 +68,7 @@ __device__ __forceinline__ uint32_t cmp2(uint32_t prev, uint32_t cur) { return c
 // ARE the level -- all on the FMA pipes (no F2I: the conversion unit is a
 // quarter-rate pipe on B200).  Levels * 4, packed.
 template <int DT>
-__device__ __forceinline__ uint32_t pack_pow2_sat(const typename Pair<DT>::T& v, float inv, float Mf)
+__device__ __forceinline__ uint32_t pack_pow2_sat(const typename Pair<DT>::T& v, float inv, float Mf, uint32_t four)
 {
     const float a = __saturatef((float)v.x * inv);
     const float b = __saturatef((float)v.y * inv);
@@ -78,7 +78,7 @@ __device__ __forceinline__ uint32_t pack_pow2_sat(const typename Pair<DT>::T& v,
     unsigned long long y, z;
     asm("fma.rm.f32x2 %0, %1, %2, %3;" : "=l"(y) : "l"(ab), "l"(m2), "l"(0x3F0000003F000000ull));
     asm("add.rm.f32x2 %0, %1, %2;" : "=l"(z) : "l"(y), "l"(0x4B0000004B000000ull));
-    return __byte_perm((uint32_t)z, (uint32_t)(z >> 32), 0x5410) * 4u + LINES_SB2;
+    return __byte_perm((uint32_t)z, (uint32_t)(z >> 32), 0x5410) * four + LINES_SB2;  // IMAD: FMA pipe
 }
 
 // Shared-memory increments of both 16-bit halves of a packed address.  No
@@ -132,7 +132,7 @@ __host__ __device__ inline int lines_end(int hs, bool) { return LINES_PLUS + LIN
 // a chunk [ia, ib).  Shared memory (lines_end): signature rows at 0, the
 // plus / minus rows of the EC events of the B/C/D lines (and of the A lines
 // unless FOLD) at LINES_PLUS / LINES_PLUS + LINES_MINUS.
-template <int DT, int QM, bool VEC, int R, bool FOLD, int DS, bool ROWFIX>
+template <int DT, int QM, bool VEC, int R, bool FOLD, int DS, bool EDGE>
 __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restrict__ buf, const LGeo& g,
                                            const QuantDev& q, const float* __restrict__ tt, char* __restrict__ h,
                                            int64_t ia, int64_t ib, int j0, int k0, int lane)
@@ -148,6 +148,9 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
     const uint32_t sent4 = (uint32_t)(g.M + 1) * 4u;
     const uint32_t S2 = sent4 * 0x10001u + LINES_SB2;  // sentinel level word (with the shared base)
     const uint32_t hk = (uint32_t)g.hk;  // signature row stride / 255
+    // 1 and -1 as registers ptxas cannot see through: the adds below stay
+    // IMADs on the FMA pipe instead of IADD3 on the (saturated) ALU pipe
+    const uint32_t ONE = g.one, MONE = 0u - g.one;
     const float Mf = (float)g.M;
     const int kk = k0 - 2 + 2 * lane;
     const bool computes = lane >= 1 && lane <= 30;
@@ -160,17 +163,17 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
     // Absent cells (outside the field) read as the sentinel:
     // * planes t = -1 .. n (plane ia-1+t) exist iff t_lo <= t < t_hi (warp-
     //   uniform; only the first two and the last plane of the field);
-    // * columns: each lane loads a CLAMPED in-row pair (always valid memory)
-    //   and masks absent cells per 16-bit half (lanekeep, one LOP3 per row);
-    // * rows: warp strips at the j boundary (rowfix, warp-uniform) predicate
-    //   their row loads and overwrite absent rows.
+    // * EDGE strips (at the j or k boundary; a separate launch) load CLAMPED
+    //   in-row pairs (always valid memory), mask absent cells per 16-bit half
+    //   (lanekeep) and predicate / overwrite absent rows.  Interior strips do
+    //   none of it.
     const int t_lo = (int)max((int64_t)-1, 1 - ia);
     const int t_hi = (int)min((int64_t)(n + 2), g.H - ia + 1);
     const bool okx = kk >= 0 && kk < (int)g.D, oky = kk + 1 >= 0 && kk + 1 < (int)g.D;
     const uint32_t lanekeep = (okx ? 0x0000FFFFu : 0u) | (oky ? 0xFFFF0000u : 0u);
-    const int kc = VEC ? min(max(kk, 0), (int)g.D - 2) : min(max(kk, 0), (int)g.D - 1);
+    const int kc = !EDGE ? kk : VEC ? min(max(kk, 0), (int)g.D - 2) : min(max(kk, 0), (int)g.D - 1);
     uint32_t rowok = (1u << NR) - 1u;
-    if constexpr (ROWFIX) {
+    if constexpr (EDGE) {
         rowok = 0;
 #pragma unroll
         for (int r = 0; r < NR; ++r) rowok |= (j0 - 1 + r >= 0 && j0 - 1 + r < (int)g.W) ? 1u << r : 0u;
@@ -180,13 +183,13 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
 
     auto fetch = [&](int t, const T* at, P2(&dst)[NR]) {
         if (t >= t_lo && t < t_hi) {
-            if constexpr (ROWFIX) {
+            if constexpr (EDGE) {
 #pragma unroll
                 for (int r = 0; r < NR; ++r)
                     if ((rowok >> r) & 1u) dst[r] = load_pair<DT, VEC>(at + r * Di, true, kk + 1 < (int)g.D);
             } else {
 #pragma unroll
-                for (int r = 0; r < NR; ++r) dst[r] = load_pair<DT, VEC>(at + r * Di, true, kk + 1 < (int)g.D);
+                for (int r = 0; r < NR; ++r) dst[r] = load_pair<DT, VEC>(at + r * Di, true, true);
             }
         }
     };
@@ -196,12 +199,12 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
         for (int r = 0; r < NR; ++r) {
             uint32_t v;
             if constexpr (QM == FT_Q_POW2)
-                v = pack_pow2_sat<DT>(src[r], q.inv, Mf);
+                v = pack_pow2_sat<DT>(src[r], q.inv, Mf, g.four);
             else
                 v = pack_pair<DT, QM, 0>(src[r], true, true, tt, q, g.M, sent4) + LINES_SB2;
-            V[r] = (v & lanekeep) | (S2 & ~lanekeep);
+            V[r] = EDGE ? (v & lanekeep) | (S2 & ~lanekeep) : v;
         }
-        if constexpr (ROWFIX) {
+        if constexpr (EDGE) {
 #pragma unroll
             for (int r = 0; r < NR; ++r)
                 if (!((rowok >> r) & 1u)) V[r] = S2;
@@ -213,12 +216,12 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
             for (int r = 0; r < NR; ++r) {
                 uint32_t v;
                 if constexpr (QM == FT_Q_POW2)
-                    v = pack_pow2_sat<DT>(src[r], q.inv, Mf);
+                    v = pack_pow2_sat<DT>(src[r], q.inv, Mf, g.four);
                 else
                     v = pack_pair<DT, QM, 0>(src[r], true, true, tt, q, g.M, sent4) + LINES_SB2;
-                V[r] = (v & lanekeep) | (S2 & ~lanekeep);
+                V[r] = EDGE ? (v & lanekeep) | (S2 & ~lanekeep) : v;
             }
-            if constexpr (ROWFIX) {
+            if constexpr (EDGE) {
 #pragma unroll
                 for (int r = 0; r < NR; ++r)
                     if (!((rowok >> r) & 1u)) V[r] = S2;
@@ -284,18 +287,23 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
             // signature of the plane-(p-1) cell: "face neighbour n activates
             // first" = bit 15 / 31 of c' - n + k (k = 0 for -side, -1 for +side)
             const uint32_t cb = o.pV[r] | 0x80008000u;
-            const uint32_t t1 = r == 1 ? hff(cb - o.pV[0]) : FF2 - tpj;  // -j
-            const uint32_t t2 = hff(cb - o.pWm[r]);                      // -k
-            const uint32_t t3 = hff(cb - W_ - 0x10001u);                 // +i
-            const uint32_t t4 = hff(cb - o.pV[r + 1] - 0x10001u);        // +j
+            const uint32_t cb1 = cb * ONE + 0xFFFEFFFFu;                      // cb - 0x10001
+            const uint32_t t1 = r == 1 ? hff(cb - o.pV[0]) : tpj * MONE + FF2;  // -j
+            const uint32_t t2 = hff(o.pWm[r] * MONE + cb);                      // -k
+            const uint32_t t3 = hff(W_ * MONE + cb1);                           // +i
+            const uint32_t t4 = hff(o.pV[r + 1] * MONE + cb1);                  // +j
             // +k: "right neighbour first" is the complement of the right
             // neighbour's -k term (lo: this word's hi half, hi: the next lane's lo)
-            const uint32_t t5 = FF2 - shift_pair(t2, __shfl_down_sync(FULL, t2, 1));
+            const uint32_t t5 = shift_pair(t2, __shfl_down_sync(FULL, t2, 1)) * MONE + FF2;
             uint32_t evS;
             if constexpr (FOLD) {
                 // row u + 7 (s_i + 1) = (t1 + t2 + t4 + t5) + 14 - 6 (tmi + t3), in
                 // units of 255; no half borrows: 14 - 6 n_i >= 2
-                const uint32_t row = (o.tmi[r] + t3) * (uint32_t)(-6) + (t1 + t2 + t4 + t5 + 14u * FF2);
+                uint32_t sum = t1 * ONE + 14u * FF2;
+                sum = t2 * ONE + sum;
+                sum = t4 * ONE + sum;
+                sum = t5 * ONE + sum;
+                const uint32_t row = (o.tmi[r] * ONE + t3) * (uint32_t)(-6) + sum;
                 evS = row * hk + o.pV[r];
             } else {
                 evS = (o.tmi[r] + t1 + t2 + t3 + t4 + t5) * hk + o.pV[r];
@@ -313,7 +321,7 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
             sinc2<LINES_PLUS>(ev_sel((o.eB[r] ^ nB) & lmask, o.pB[r] | (nB & 0x80008000u), dummy2));
             sinc2<LINES_PLUS>(ev_sel((o.eC[r] ^ nC) & lmask, o.pC[r] | (nC & 0x80008000u), dummy2));
             sinc2<LINES_PLUS>(ev_sel((o.eD[r] ^ nD) & lmask, o.pD[r] | (~nD & 0x80008000u), dummy2));
-            x.tmi[r] = FF2 - t3;
+            x.tmi[r] = t3 * MONE + FF2;
             tpj = t4;
             x.pWm[r] = Wm[r];
             x.pB[r] = B;
@@ -357,11 +365,12 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
     }
 }
 
-// ROWFIX = false: every warp strip whose rows j0-1 .. j0+R all lie in the
-// field (columns and planes are masked in-line); ROWFIX = true: the few strips
-// at the j boundary, with row-predicated loads.  Two launches rather than a
-// branch, so that the boundary code cannot cost the main loop registers.
-template <int DT, int QM, bool VEC, int R, bool FOLD, int DS, bool ROWFIX>
+// EDGE = false: every warp strip whose rows j0-1 .. j0+R and cells
+// k0-2 .. k0+61 all lie in the field; EDGE = true: the strips at the j or k
+// boundary (one warp per strip-chunk; masked columns, predicated rows).  Two
+// launches rather than a branch, so that the boundary code cannot cost the
+// main loop registers or instructions.
+template <int DT, int QM, bool VEC, int R, bool FOLD, int DS, bool EDGE>
 __global__ void __launch_bounds__(LINES_NTH, LINES_MINB) lines3d_kernel(const typename Elem<DT>::T* __restrict__ buf,
                                                                         LGeo g, QuantDev q,
                                                                         unsigned long long* __restrict__ hist)
@@ -380,19 +389,31 @@ __global__ void __launch_bounds__(LINES_NTH, LINES_MINB) lines3d_kernel(const ty
 
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x / 32;
-    if constexpr (ROWFIX) {
-        // one warp per (chunk, column tile, row-boundary strip): these strips are
-        // few, so they are spread over all warps of the grid
+    if constexpr (EDGE) {
+        // one warp per (chunk, edge strip); per chunk: every strip of the
+        // k-boundary column tiles [0, kb_lo) and [tiles_k - kb_hi, tiles_k),
+        // then the row-boundary strips (rf_j0) of the other column tiles
         const int64_t nw = (int64_t)gridDim.x * (LINES_NTH / 32);
-        const int64_t per_chunk = (int64_t)g.tiles_k * g.rf_n;
+        const int nstrips = (int)(g.W / R) + 1;  // j0 = 0, R, .. <= W
+        const int nkb = g.kb_lo + g.kb_hi;
+        const int64_t n1 = (int64_t)nkb * nstrips;
+        const int64_t per_chunk = n1 + (int64_t)(g.tiles_k - nkb) * g.rf_n;
         for (int64_t it = (int64_t)blockIdx.x * (LINES_NTH / 32) + warp; it < g.n_items; it += nw) {
             const int64_t ch = it / per_chunk;
-            const int rem = (int)(it - ch * per_chunk);
-            const int j0 = g.rf_j0[rem % g.rf_n];
-            const int k0 = (rem / g.rf_n) * 60;
+            const int64_t rem = it - ch * per_chunk;
+            int j0, tk;
+            if (rem < n1) {
+                const int c = (int)(rem / nstrips);
+                tk = c < g.kb_lo ? c : g.tiles_k - g.kb_hi + (c - g.kb_lo);
+                j0 = (int)(rem % nstrips) * R;
+            } else {
+                const int e = (int)(rem - n1);
+                tk = g.kb_lo + e / g.rf_n;
+                j0 = g.rf_j0[e % g.rf_n];
+            }
             const int64_t ia = g.v0 + ch * g.chunk;
             const int64_t ib = min(ia + (int64_t)g.chunk, g.v1);
-            lines_item<DT, QM, VEC, R, FOLD, DS, true>(buf, g, q, tt, h, ia, ib, j0, k0, lane);
+            lines_item<DT, QM, VEC, R, FOLD, DS, true>(buf, g, q, tt, h, ia, ib, j0, tk * 60, lane);
         }
     } else {
         const int64_t per_chunk = (int64_t)g.tiles_j * g.tiles_k;
@@ -401,7 +422,8 @@ __global__ void __launch_bounds__(LINES_NTH, LINES_MINB) lines3d_kernel(const ty
             const int rem = (int)(item - ch * per_chunk);
             const int j0 = (rem / g.tiles_k) * ((LINES_NTH / 32) * R) + warp * R;
             const int k0 = (rem % g.tiles_k) * 60;
-            if (!(j0 >= 1 && j0 + R < g.W)) continue;  // past the lattice or a row-boundary strip
+            // edge strips (and strips past the lattice) belong to the other launch
+            if (!(j0 >= 1 && j0 + R < g.W && k0 >= 2 && k0 + 62 <= g.D)) continue;
             const int64_t ia = g.v0 + ch * g.chunk;
             const int64_t ib = min(ia + (int64_t)g.chunk, g.v1);
             lines_item<DT, QM, VEC, R, FOLD, DS, false>(buf, g, q, tt, h, ia, ib, j0, k0, lane);
@@ -474,27 +496,30 @@ static int lines_chunk(int64_t rows, int64_t tiles, int64_t ctas)
     return (int)cdiv(rows, nchunks);
 }
 
-template <int DT, int QM, bool VEC, bool FOLD, int DS, bool ROWFIX>
+template <int DT, int QM, bool VEC, bool FOLD, int DS, bool EDGE>
 static int launch_lines_kernel(const ft_window* win, LGeo g, const QuantDev& qd, size_t smem, uint64_t* hist,
                                cudaStream_t st)
 {
     using T = typename Elem<DT>::T;
-    auto kern = lines3d_kernel<DT, QM, VEC, LINES_R, FOLD, DS, ROWFIX>;
+    auto kern = lines3d_kernel<DT, QM, VEC, LINES_R, FOLD, DS, EDGE>;
     FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     FT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, LINES_NTH, smem));
     if (per_sm < 1) return FT_ERR_ARG;
     const int64_t cap = (int64_t)nsm_l() * per_sm;
     int64_t grid;
-    if (ROWFIX) {
+    if (EDGE) {
         // row-boundary strips: j0 = 0 and every strip reaching row W-1 or past it
         g.rf_n = 0;
         for (int64_t j0 = 0; j0 <= g.W && g.rf_n < 4; j0 += LINES_R)
             if (j0 < 1 || j0 + LINES_R >= g.W) g.rf_j0[g.rf_n++] = (int)j0;
-        if (g.rf_n == 0) return FT_OK;
-        if (g.rf_n == 4 && g.W > 3 * LINES_R) return FT_ERR_ARG;  // unreachable: at most 3 strips
+        // k-boundary column tiles: k0 < 2 (tile 0) and k0 + 62 > D (the last ones)
+        g.kb_lo = 1;
+        g.kb_hi = 0;
+        for (int tk = g.tiles_k - 1; tk >= 1 && tk * 60 + 62 > g.D; --tk) ++g.kb_hi;
+        const int64_t nstrips = g.W / LINES_R + 1;
+        const int64_t strips = (int64_t)(g.kb_lo + g.kb_hi) * nstrips + (int64_t)(g.tiles_k - g.kb_lo - g.kb_hi) * g.rf_n;
         // one warp per strip-chunk: chunks short enough to fill the grid's warps
-        const int64_t strips = (int64_t)g.tiles_k * g.rf_n;
         g.chunk = lines_chunk(g.v1 - g.v0, cdiv(strips, LINES_NTH / 32), cap);
         g.n_items = strips * cdiv(g.v1 - g.v0, g.chunk);
         grid = std::min<int64_t>(cap, cdiv(g.n_items, LINES_NTH / 32));
@@ -542,6 +567,8 @@ static int launch_lines3d(const ft_window* win, int64_t H, int64_t W, int64_t D,
     g.H = H; g.W = W; g.D = D; g.v0 = v0; g.v1 = v1; g.first = win->first; g.M = M;
     g.hs = lines_hs(M);
     g.hk = g.hs / 255;
+    g.one = 1;
+    g.four = 4;
     const bool vec = D % 2 == 0 && reinterpret_cast<uintptr_t>(win->data) % (2 * sizeof(T)) == 0;
     const bool fold = lines_fold_ok(M, g.hs);
     const size_t smem = (size_t)lines_end(g.hs, fold);

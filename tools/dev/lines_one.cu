@@ -5,8 +5,8 @@
 #ifndef DEV_FOLD
 #define DEV_FOLD true
 #endif
-#ifndef DEV_ROWFIX
-#define DEV_ROWFIX false
+#ifndef DEV_EDGE
+#define DEV_EDGE false
 #endif
 #ifndef DEV_DS
 #define DEV_DS 2048
@@ -14,5 +14,5 @@
 #ifndef DEV_GUARD
 #define DEV_GUARD false
 #endif
-template __global__ void ft::lines3d_kernel<FT_F32, FT_Q_POW2, true, ft::LINES_R, DEV_FOLD, DEV_DS, DEV_ROWFIX>(const float*, ft::LGeo, ft::QuantDev,
+template __global__ void ft::lines3d_kernel<FT_F32, FT_Q_POW2, true, ft::LINES_R, DEV_FOLD, DEV_DS, DEV_EDGE>(const float*, ft::LGeo, ft::QuantDev,
                                                                                    unsigned long long*);
