@@ -25,6 +25,8 @@ struct LGeo {
     int hk;                          // ft_lines3d: signature row stride / 255
     int rf_n, rf_j0[4];              // ft_lines3d: the row-boundary warp strips (j0 values)
     int kb_lo, kb_hi;                // ft_lines3d: k-boundary column tiles at each end
+    int e_chunk;                     // ft_lines3d: planes per boundary warp item
+    int64_t e_items;                 // ft_lines3d: boundary warp items
     uint32_t one, four;              // ft_lines3d: 1 and 4 as opaque registers (IMAD, not IADD3/LEA)
 };
 

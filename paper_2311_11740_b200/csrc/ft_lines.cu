@@ -89,13 +89,28 @@ __device__ __forceinline__ uint32_t pack_pow2_sat(const typename Pair<DT>::T& v,
 // Packed level words carry the shared address of the block (LINES_SBASE, in
 // every half), so a half IS the shared address of a signature bin and the
 // plus/minus rows are an immediate above it: ATOMS [R + imm], no base add.
+#ifndef LINES_DEV_NOATOM
+#define LINES_DEV_NOATOM 0  // dev timing only (wrong results): bit 0 drops the dense, bit 1 the sparse ATOMS
+#endif
 template <int OFF>
 __device__ __forceinline__ void sinc2(uint32_t addr)
 {
     const uint32_t hi = __umulhi(addr, 0x10000u);
     const uint32_t lo = addr - hi * 0x10000u;
-    asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(lo), "n"(OFF));
-    asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(hi), "n"(OFF));
+    if constexpr ((LINES_DEV_NOATOM >> (OFF == 0 ? 0 : 1)) & 1) {
+        asm volatile("" ::"r"(lo), "r"(hi));
+    } else {
+        asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(lo), "n"(OFF));
+        asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(hi), "n"(OFF));
+    }
+}
+// (a & m) | (b & ~m) as ONE LOP3 (left to itself ptxas sometimes splits it
+// into two around a hoisted b & ~m)
+__device__ __forceinline__ uint32_t sel_mask(uint32_t m, uint32_t a, uint32_t b)
+{
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0xCA;" : "=r"(d) : "r"(m), "r"(a), "r"(b));
+    return d;
 }
 // halves of addr whose flag bit (15 / 31) is set, dummy2's halves elsewhere
 __device__ __forceinline__ uint32_t ev_sel(uint32_t flags, uint32_t addr, uint32_t dummy2)
@@ -104,7 +119,7 @@ __device__ __forceinline__ uint32_t ev_sel(uint32_t flags, uint32_t addr, uint32
     // mode; the __byte_perm intrinsic masks the selector to 3 bits)
     uint32_t m;
     asm("prmt.b32 %0, %1, 0, 0xBB99;" : "=r"(m) : "r"(flags));
-    return (addr & m) | (dummy2 & ~m);
+    return sel_mask(m, addr, dummy2);
 }
 
 #ifndef LINES_NTH_DEF
@@ -128,11 +143,13 @@ __host__ __device__ inline int lines_nsig(bool fold) { return fold ? 21 : 7; }
 constexpr int LINES_PLUS = 65536;
 __host__ __device__ inline int lines_end(int hs, bool) { return LINES_PLUS + LINES_MINUS + hs; }
 
-// One warp strip (R lattice rows x 60 lattice columns) marching the planes of
+// One warp strip (R lattice rows x 62 lattice columns) marching the planes of
 // a chunk [ia, ib).  Shared memory (lines_end): signature rows at 0, the
 // plus / minus rows of the EC events of the B/C/D lines (and of the A lines
 // unless FOLD) at LINES_PLUS / LINES_PLUS + LINES_MINUS.
-template <int DT, int QM, bool VEC, int R, bool FOLD, int DS, bool EDGE>
+// EDGE 0: interior strip (no guards); 1: every row present, columns outside
+// the field (clamped loads, masked halves); 2: rows and columns guarded.
+template <int DT, int QM, bool VEC, int R, bool FOLD, int DS, int EDGE>
 __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restrict__ buf, const LGeo& g,
                                            const QuantDev& q, const float* __restrict__ tt, char* __restrict__ h,
                                            int64_t ia, int64_t ib, int j0, int k0, int lane)
@@ -152,28 +169,31 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
     // IMADs on the FMA pipe instead of IADD3 on the (saturated) ALU pipe
     const uint32_t ONE = g.one, MONE = 0u - g.one;
     const float Mf = (float)g.M;
-    const int kk = k0 - 2 + 2 * lane;
-    const bool computes = lane >= 1 && lane <= 30;
-    // halo lanes 0 / 31 book nothing; through a shuffle so that ptxas keeps a
-    // mask register (one 3-input LOP3) instead of SEL on a predicate
-    const uint32_t lmask = __shfl_sync(FULL, computes ? FULL : 0u, lane);
+    // lane l holds cells kk, kk+1 (kk even: aligned pair loads); lattice
+    // columns k0 .. k0+61 are computed by lane 0's high half, both halves of
+    // lanes 1 .. 30 and lane 31's low half (the other two halves are the halo:
+    // lane 0's low cell feeds the -k neighbour, lane 31's high cell the +k one)
+    const int kk = k0 - 1 + 2 * lane;
+    // through a shuffle so that ptxas keeps a mask register (one 3-input LOP3)
+    // instead of SEL on a predicate
+    const uint32_t lmask = __shfl_sync(FULL, lane == 0 ? 0xFFFF0000u : lane == 31 ? 0x0000FFFFu : FULL, lane);
     const uint32_t dummy2 = S2;    // sentinel bin (never read) of signature row 0 / the plus row
     const int n = (int)(ib - ia);
 
     // Absent cells (outside the field) read as the sentinel:
     // * planes t = -1 .. n (plane ia-1+t) exist iff t_lo <= t < t_hi (warp-
     //   uniform; only the first two and the last plane of the field);
-    // * EDGE strips (at the j or k boundary; a separate launch) load CLAMPED
-    //   in-row pairs (always valid memory), mask absent cells per 16-bit half
-    //   (lanekeep) and predicate / overwrite absent rows.  Interior strips do
-    //   none of it.
+    // * EDGE strips (at the k boundary) load CLAMPED in-row pairs (always
+    //   valid memory) and mask absent cells per 16-bit half (lanekeep); at the
+    //   j boundary (EDGE 2) they also predicate / overwrite absent rows.
+    //   Interior strips do none of it.
     const int t_lo = (int)max((int64_t)-1, 1 - ia);
     const int t_hi = (int)min((int64_t)(n + 2), g.H - ia + 1);
     const bool okx = kk >= 0 && kk < (int)g.D, oky = kk + 1 >= 0 && kk + 1 < (int)g.D;
     const uint32_t lanekeep = (okx ? 0x0000FFFFu : 0u) | (oky ? 0xFFFF0000u : 0u);
-    const int kc = !EDGE ? kk : VEC ? min(max(kk, 0), (int)g.D - 2) : min(max(kk, 0), (int)g.D - 1);
+    const int kc = EDGE == 0 ? kk : VEC ? min(max(kk, 0), (int)g.D - 2) : min(max(kk, 0), (int)g.D - 1);
     uint32_t rowok = (1u << NR) - 1u;
-    if constexpr (EDGE) {
+    if constexpr (EDGE == 2) {
         rowok = 0;
 #pragma unroll
         for (int r = 0; r < NR; ++r) rowok |= (j0 - 1 + r >= 0 && j0 - 1 + r < (int)g.W) ? 1u << r : 0u;
@@ -183,10 +203,13 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
 
     auto fetch = [&](int t, const T* at, P2(&dst)[NR]) {
         if (t >= t_lo && t < t_hi) {
-            if constexpr (EDGE) {
+            if constexpr (EDGE == 2) {
 #pragma unroll
                 for (int r = 0; r < NR; ++r)
                     if ((rowok >> r) & 1u) dst[r] = load_pair<DT, VEC>(at + r * Di, true, kk + 1 < (int)g.D);
+            } else if constexpr (EDGE == 1) {
+#pragma unroll
+                for (int r = 0; r < NR; ++r) dst[r] = load_pair<DT, VEC>(at + r * Di, true, kk + 1 < (int)g.D);
             } else {
 #pragma unroll
                 for (int r = 0; r < NR; ++r) dst[r] = load_pair<DT, VEC>(at + r * Di, true, true);
@@ -202,9 +225,9 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
                 v = pack_pow2_sat<DT>(src[r], q.inv, Mf, g.four);
             else
                 v = pack_pair<DT, QM, 0>(src[r], true, true, tt, q, g.M, sent4) + LINES_SB2;
-            V[r] = EDGE ? (v & lanekeep) | (S2 & ~lanekeep) : v;
+            V[r] = EDGE ? sel_mask(lanekeep, v, S2) : v;
         }
-        if constexpr (EDGE) {
+        if constexpr (EDGE == 2) {
 #pragma unroll
             for (int r = 0; r < NR; ++r)
                 if (!((rowok >> r) & 1u)) V[r] = S2;
@@ -219,9 +242,9 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
                     v = pack_pow2_sat<DT>(src[r], q.inv, Mf, g.four);
                 else
                     v = pack_pair<DT, QM, 0>(src[r], true, true, tt, q, g.M, sent4) + LINES_SB2;
-                V[r] = EDGE ? (v & lanekeep) | (S2 & ~lanekeep) : v;
+                V[r] = EDGE ? sel_mask(lanekeep, v, S2) : v;
             }
-            if constexpr (EDGE) {
+            if constexpr (EDGE == 2) {
 #pragma unroll
                 for (int r = 0; r < NR; ++r)
                     if (!((rowok >> r) & 1u)) V[r] = S2;
@@ -312,7 +335,7 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
                 const uint32_t aA = o.pV[r] | ((t3 << 8) & 0x80008000u);
                 sinc2<LINES_PLUS>(ev_sel(fA << 8, aA, dummy2));
             }
-            sinc2<0>((evS & lmask) | (dummy2 & ~lmask));  // halo lanes: sentinel bin of row 0
+            sinc2<0>(sel_mask(lmask, evS, dummy2));  // halo lanes: sentinel bin of row 0
             // B / C / D lines: event iff the along-i order flips at p-1; sign -1
             // (B, C): local min -> minus row; sign +1 (D): local max -> minus row
             const uint32_t B = vmin2(V[r - 1], W_);
@@ -365,12 +388,37 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
     }
 }
 
-// EDGE = false: every warp strip whose rows j0-1 .. j0+R and cells
-// k0-2 .. k0+61 all lie in the field; EDGE = true: the strips at the j or k
-// boundary (one warp per strip-chunk; masked columns, predicated rows).  Two
-// launches rather than a branch, so that the boundary code cannot cost the
-// main loop registers or instructions.
-template <int DT, int QM, bool VEC, int R, bool FOLD, int DS, bool EDGE>
+// The CTA tiles (TJ = 16 R rows x 62 columns) of ntk column tiles, rows up to
+// the last tile holding an interior strip, times the planes, as ONE linear
+// range cut evenly over the CTAs: every CTA marches the same number of
+// tile-planes (segments of consecutive planes of one tile), so no CTA waits
+// on a quantised item count.  Warp strips with rows outside 1 .. W-1 are left
+// to the warp loop.  f(j0, column tile, ia, ib).
+template <int R, typename F>
+__device__ __forceinline__ void cta_tiles(const LGeo& g, int ntk, int64_t np, int warp, F&& f)
+{
+    constexpr int TJ = (LINES_NTH / 32) * R;
+    const int64_t T = (int64_t)g.tiles_j * ntk * np;
+    const int64_t u_end = T * (blockIdx.x + 1) / gridDim.x;
+    for (int64_t u = T * blockIdx.x / gridDim.x; u < u_end;) {
+        const int tile = (int)(u / np);
+        const int64_t p = u - (int64_t)tile * np;
+        const int64_t seg = min(u_end - u, np - p);
+        u += seg;
+        const int tj = tile / ntk;
+        const int j0 = tj * TJ + warp * R;
+        if (!(j0 >= 1 && j0 + R < g.W)) continue;  // the warp loop's
+        f(j0, tile - tj * ntk, g.v0 + p, g.v0 + p + seg);
+    }
+}
+
+// Work split.  MODE 0 / 2: (A) the CTA tiles of the interior column tiles
+// (guard-free march), then (B) those of the k-boundary column tiles (column-
+// guarded march), each cut evenly over the CTAs (cta_tiles).  MODE 1 / 2: (C)
+// the row-boundary strips, one warp per strip-chunk (fully guarded march).
+// Separate loops, separate instantiations of lines_item: the boundary code
+// costs the interior march no instructions or registers.
+template <int DT, int QM, bool VEC, int R, bool FOLD, int DS, int MODE>
 __global__ void __launch_bounds__(LINES_NTH, LINES_MINB) lines3d_kernel(const typename Elem<DT>::T* __restrict__ buf,
                                                                         LGeo g, QuantDev q,
                                                                         unsigned long long* __restrict__ hist)
@@ -389,44 +437,31 @@ __global__ void __launch_bounds__(LINES_NTH, LINES_MINB) lines3d_kernel(const ty
 
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x / 32;
-    if constexpr (EDGE) {
-        // one warp per (chunk, edge strip); per chunk: every strip of the
-        // k-boundary column tiles [0, kb_lo) and [tiles_k - kb_hi, tiles_k),
-        // then the row-boundary strips (rf_j0) of the other column tiles
+    if constexpr (MODE != 1) {
+        // A: interior column tiles; B: the k-boundary ones (EDGE 1 march)
+        const int64_t np = g.v1 - g.v0;
+        const int ntk = g.tiles_k - g.kb_lo - g.kb_hi;
+        cta_tiles<R>(g, ntk, np, warp, [&](int j0, int tk, int64_t ia, int64_t ib) {
+            lines_item<DT, QM, VEC, R, FOLD, DS, 0>(buf, g, q, tt, h, ia, ib, j0, (g.kb_lo + tk) * 62 - 1, lane);
+        });
+        cta_tiles<R>(g, g.kb_lo + g.kb_hi, np, warp, [&](int j0, int tk, int64_t ia, int64_t ib) {
+            const int t = tk < g.kb_lo ? tk : g.tiles_k - g.kb_hi + (tk - g.kb_lo);
+            lines_item<DT, QM, VEC, R, FOLD, DS, 1>(buf, g, q, tt, h, ia, ib, j0, t * 62 - 1, lane);
+        });
+    }
+    if constexpr (MODE != 0) {
+        // C: the row-boundary strips (rf_j0: j0 = 0 and the strips reaching
+        // row W-1 or past it) of every column tile
         const int64_t nw = (int64_t)gridDim.x * (LINES_NTH / 32);
-        const int nstrips = (int)(g.W / R) + 1;  // j0 = 0, R, .. <= W
-        const int nkb = g.kb_lo + g.kb_hi;
-        const int64_t n1 = (int64_t)nkb * nstrips;
-        const int64_t per_chunk = n1 + (int64_t)(g.tiles_k - nkb) * g.rf_n;
-        for (int64_t it = (int64_t)blockIdx.x * (LINES_NTH / 32) + warp; it < g.n_items; it += nw) {
+        const int64_t per_chunk = (int64_t)g.tiles_k * g.rf_n;
+        for (int64_t it = (int64_t)blockIdx.x * (LINES_NTH / 32) + warp; it < g.e_items; it += nw) {
             const int64_t ch = it / per_chunk;
-            const int64_t rem = it - ch * per_chunk;
-            int j0, tk;
-            if (rem < n1) {
-                const int c = (int)(rem / nstrips);
-                tk = c < g.kb_lo ? c : g.tiles_k - g.kb_hi + (c - g.kb_lo);
-                j0 = (int)(rem % nstrips) * R;
-            } else {
-                const int e = (int)(rem - n1);
-                tk = g.kb_lo + e / g.rf_n;
-                j0 = g.rf_j0[e % g.rf_n];
-            }
-            const int64_t ia = g.v0 + ch * g.chunk;
-            const int64_t ib = min(ia + (int64_t)g.chunk, g.v1);
-            lines_item<DT, QM, VEC, R, FOLD, DS, true>(buf, g, q, tt, h, ia, ib, j0, tk * 60, lane);
-        }
-    } else {
-        const int64_t per_chunk = (int64_t)g.tiles_j * g.tiles_k;
-        for (int64_t item = blockIdx.x; item < g.n_items; item += gridDim.x) {
-            const int64_t ch = item / per_chunk;
-            const int rem = (int)(item - ch * per_chunk);
-            const int j0 = (rem / g.tiles_k) * ((LINES_NTH / 32) * R) + warp * R;
-            const int k0 = (rem % g.tiles_k) * 60;
-            // edge strips (and strips past the lattice) belong to the other launch
-            if (!(j0 >= 1 && j0 + R < g.W && k0 >= 2 && k0 + 62 <= g.D)) continue;
-            const int64_t ia = g.v0 + ch * g.chunk;
-            const int64_t ib = min(ia + (int64_t)g.chunk, g.v1);
-            lines_item<DT, QM, VEC, R, FOLD, DS, false>(buf, g, q, tt, h, ia, ib, j0, k0, lane);
+            const int rem = (int)(it - ch * per_chunk);
+            const int tk = rem / g.rf_n;
+            const int j0 = g.rf_j0[rem - tk * g.rf_n];
+            const int64_t ia = g.v0 + ch * g.e_chunk;
+            const int64_t ib = min(ia + (int64_t)g.e_chunk, g.v1);
+            lines_item<DT, QM, VEC, R, FOLD, DS, 2>(buf, g, q, tt, h, ia, ib, j0, tk * 62 - 1, lane);
         }
     }
     __syncthreads();
@@ -496,39 +531,40 @@ static int lines_chunk(int64_t rows, int64_t tiles, int64_t ctas)
     return (int)cdiv(rows, nchunks);
 }
 
-template <int DT, int QM, bool VEC, bool FOLD, int DS, bool EDGE>
+#ifndef LINES_FUSED_DEF
+#define LINES_FUSED_DEF 1
+#endif
+// Interior and boundary items in one launch (MODE 2) or two (dev A/B)
+template <int DT, int QM, bool VEC, bool FOLD, int DS, int MODE>
 static int launch_lines_kernel(const ft_window* win, LGeo g, const QuantDev& qd, size_t smem, uint64_t* hist,
                                cudaStream_t st)
 {
     using T = typename Elem<DT>::T;
-    auto kern = lines3d_kernel<DT, QM, VEC, LINES_R, FOLD, DS, EDGE>;
+    auto kern = lines3d_kernel<DT, QM, VEC, LINES_R, FOLD, DS, MODE>;
     FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     FT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, LINES_NTH, smem));
     if (per_sm < 1) return FT_ERR_ARG;
     const int64_t cap = (int64_t)nsm_l() * per_sm;
-    int64_t grid;
-    if (EDGE) {
-        // row-boundary strips: j0 = 0 and every strip reaching row W-1 or past it
-        g.rf_n = 0;
-        for (int64_t j0 = 0; j0 <= g.W && g.rf_n < 4; j0 += LINES_R)
-            if (j0 < 1 || j0 + LINES_R >= g.W) g.rf_j0[g.rf_n++] = (int)j0;
-        // k-boundary column tiles: k0 < 2 (tile 0) and k0 + 62 > D (the last ones)
-        g.kb_lo = 1;
-        g.kb_hi = 0;
-        for (int tk = g.tiles_k - 1; tk >= 1 && tk * 60 + 62 > g.D; --tk) ++g.kb_hi;
-        const int64_t nstrips = g.W / LINES_R + 1;
-        const int64_t strips = (int64_t)(g.kb_lo + g.kb_hi) * nstrips + (int64_t)(g.tiles_k - g.kb_lo - g.kb_hi) * g.rf_n;
-        // one warp per strip-chunk: chunks short enough to fill the grid's warps
-        g.chunk = lines_chunk(g.v1 - g.v0, cdiv(strips, LINES_NTH / 32), cap);
-        g.n_items = strips * cdiv(g.v1 - g.v0, g.chunk);
-        grid = std::min<int64_t>(cap, cdiv(g.n_items, LINES_NTH / 32));
-    } else {
-        const int64_t tiles = (int64_t)g.tiles_j * g.tiles_k;
-        g.chunk = lines_chunk(g.v1 - g.v0, tiles, cap);
-        g.n_items = tiles * cdiv(g.v1 - g.v0, g.chunk);
-        grid = std::min<int64_t>(cap, g.n_items);
-    }
+    // CTA tiles: column tiles x row tiles up to the last interior strip
+    // (j0 + R < W); k-boundary column tiles: k0 < 1 (tile 0), k0 + 63 > D
+    constexpr int TJ = (LINES_NTH / 32) * LINES_R;
+    g.kb_lo = 1;
+    g.kb_hi = 0;
+    for (int tk = g.tiles_k - 1; tk >= 1 && tk * 62 + 62 > g.D; --tk) ++g.kb_hi;
+    g.tiles_j = g.W > LINES_R ? (int)((g.W - LINES_R - 1) / TJ + 1) : 0;
+    const int64_t np = g.v1 - g.v0;
+    const int64_t work = MODE == 1 ? 0 : (int64_t)g.tiles_j * g.tiles_k * np;
+    // warp strips: j0 = 0 and every strip reaching row W-1 or past it
+    g.rf_n = 0;
+    for (int64_t j0 = 0; j0 <= g.W && g.rf_n < 4; j0 += LINES_R)
+        if (j0 < 1 || j0 + LINES_R >= g.W) g.rf_j0[g.rf_n++] = (int)j0;
+    const int64_t strips = (int64_t)g.tiles_k * g.rf_n;
+    // one warp per strip-chunk: chunks short enough to fill the grid's warps
+    g.e_chunk = lines_chunk(np, cdiv(strips, LINES_NTH / 32), cap);
+    g.e_items = MODE == 0 ? 0 : strips * cdiv(np, g.e_chunk);
+    // the CTA ranges: >= 32 tile-planes per CTA
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(cap, std::max<int64_t>(cdiv(work, 32), cdiv(g.e_items, LINES_NTH / 32))));
     kern<<<(int)grid, LINES_NTH, smem, st>>>(static_cast<const T*>(win->data), g, qd,
                                             reinterpret_cast<unsigned long long*>(hist));
     FT_CUDA_TRY(cudaGetLastError());
@@ -539,22 +575,31 @@ template <int DT, int QM, bool VEC, bool FOLD, int DS>
 static int launch_lines_two(const ft_window* win, const LGeo& g, const QuantDev& qd, size_t smem, uint64_t* hist,
                             cudaStream_t st)
 {
-    const int rc = launch_lines_kernel<DT, QM, VEC, FOLD, DS, false>(win, g, qd, smem, hist, st);
-    return rc ? rc : launch_lines_kernel<DT, QM, VEC, FOLD, DS, true>(win, g, qd, smem, hist, st);
+    if constexpr (LINES_FUSED_DEF) {
+        return launch_lines_kernel<DT, QM, VEC, FOLD, DS, 2>(win, g, qd, smem, hist, st);
+    } else {
+        const int rc = launch_lines_kernel<DT, QM, VEC, FOLD, DS, 0>(win, g, qd, smem, hist, st);
+        return rc ? rc : launch_lines_kernel<DT, QM, VEC, FOLD, DS, 1>(win, g, qd, smem, hist, st);
+    }
 }
 
 template <int DT, int QM, bool VEC, bool FOLD>
 static int launch_lines_pair(const ft_window* win, const LGeo& g, const QuantDev& qd, size_t smem, uint64_t* hist,
                              cudaStream_t st)
 {
-    // specialised on the common row lengths (BASELINE configs)
-    switch (VEC ? g.D : 0) {
-    case 2048: return launch_lines_two<DT, QM, VEC, FOLD, 2048>(win, g, qd, smem, hist, st);
-    case 1024: return launch_lines_two<DT, QM, VEC, FOLD, 1024>(win, g, qd, smem, hist, st);
-    case 512: return launch_lines_two<DT, QM, VEC, FOLD, 512>(win, g, qd, smem, hist, st);
-    case 256: return launch_lines_two<DT, QM, VEC, FOLD, 256>(win, g, qd, smem, hist, st);
-    default: return launch_lines_two<DT, QM, VEC, FOLD, 0>(win, g, qd, smem, hist, st);
+    // specialised on the common row lengths of the BASELINE configs' f32 / u16
+    // fields (C4a / C5 f32, C4b u16); other inputs take the generic loop
+    constexpr bool spec = VEC && (DT == FT_F32 || DT == FT_U16) && QM != FT_Q_TABLE_ROBUST;
+    if constexpr (spec) {
+        switch (g.D) {
+        case 2048: return launch_lines_two<DT, QM, VEC, FOLD, 2048>(win, g, qd, smem, hist, st);
+        case 1024: return launch_lines_two<DT, QM, VEC, FOLD, 1024>(win, g, qd, smem, hist, st);
+        case 512: return launch_lines_two<DT, QM, VEC, FOLD, 512>(win, g, qd, smem, hist, st);
+        case 256: return launch_lines_two<DT, QM, VEC, FOLD, 256>(win, g, qd, smem, hist, st);
+        default: break;
+        }
     }
+    return launch_lines_two<DT, QM, VEC, FOLD, 0>(win, g, qd, smem, hist, st);
 }
 
 template <int DT, int QM>
@@ -562,7 +607,6 @@ static int launch_lines3d(const ft_window* win, int64_t H, int64_t W, int64_t D,
                           const ft_quant* qa, int32_t M, uint64_t* hist, cudaStream_t st)
 {
     using T = typename Elem<DT>::T;
-    constexpr int R = LINES_R, TJ = (LINES_NTH / 32) * R;
     LGeo g{};
     g.H = H; g.W = W; g.D = D; g.v0 = v0; g.v1 = v1; g.first = win->first; g.M = M;
     g.hs = lines_hs(M);
@@ -572,8 +616,7 @@ static int launch_lines3d(const ft_window* win, int64_t H, int64_t W, int64_t D,
     const bool vec = D % 2 == 0 && reinterpret_cast<uintptr_t>(win->data) % (2 * sizeof(T)) == 0;
     const bool fold = lines_fold_ok(M, g.hs);
     const size_t smem = (size_t)lines_end(g.hs, fold);
-    g.tiles_j = (int)cdiv(W + 1, TJ);
-    g.tiles_k = (int)cdiv(D + 1, 60);
+    g.tiles_k = (int)((D + 1) / 62 + 1);  // tile t: lattice columns 62 t - 1 .. 62 t + 60
     if (const int rc = lines_check_sbase()) return rc;
     QuantDev qd = qdev(qa);
     if (QM == FT_Q_POW2) qd.inv = M > 0 ? qd.scale / (float)M : 0.f;
@@ -603,7 +646,7 @@ extern "C" int ft_lines3d(const ft_window* win, int64_t H, int64_t W, int64_t D,
     if (win->dtype == FT_F32 && qm == FT_Q_POW2)
         return launch_lines3d<FT_F32, FT_Q_POW2>(win, H, W, D, v0, v1, q, M, hist, st);
     return FT_ERR_ARG;
-#endif
+#else
     switch (win->dtype) {
     case FT_I32:
         if (qm != FT_Q_IDENTITY) return FT_ERR_ARG;
@@ -625,6 +668,7 @@ extern "C" int ft_lines3d(const ft_window* win, int64_t H, int64_t W, int64_t D,
         return launch_lines3d<FT_F32, FT_Q_TABLE_ROBUST>(win, H, W, D, v0, v1, q, M, hist, st);
     }
     return FT_ERR_ARG;
+#endif
 }
 
 extern "C" int ft_lines3d_ok(int32_t M) { return M >= 0 && lines_ok(M) ? 1 : 0; }

@@ -102,3 +102,16 @@ def test_lines_auto_and_limits(ft, orc):
     got = ft.descriptor_curves(ft.Field3D(lv, 3000), _tabs(ft))  # auto -> lattice kernel
     for c, w in zip(got, _want(orc, ft, lv, 3000)):
         assert np.array_equal(c.numerators, w)
+
+
+@pytest.mark.parametrize("D", [61, 62, 63, 64, 123, 124, 125, 126, 127, 186, 187, 188, 189, 256, 512])
+def test_lines_column_tiles(ft, orc, D):
+    """Row lengths around the 62-column warp-strip tiling (interior / k-boundary
+    tile split, the halo halves of lanes 0 and 31) and the D-specialised
+    interior loads (256, 512), on a smooth f32 field with the pow2 quantizer."""
+    import torch
+    x = _grf((37, 70, D), 2.0, 1000 + D)
+    src = ft.DeviceSource(torch.from_numpy(x).cuda(), 511, value_range=(0.0, 1.0))
+    got = ft.descriptor_curves(src, _tabs(ft), path="lines")
+    for c, w in zip(got, _want(orc, ft, x, 511, (0.0, 1.0))):
+        assert np.array_equal(c.numerators, w)

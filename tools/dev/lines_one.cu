@@ -6,7 +6,7 @@
 #define DEV_FOLD true
 #endif
 #ifndef DEV_EDGE
-#define DEV_EDGE false
+#define DEV_EDGE 2
 #endif
 #ifndef DEV_DS
 #define DEV_DS 2048
