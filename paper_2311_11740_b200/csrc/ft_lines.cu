@@ -198,6 +198,8 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
     //   Interior strips do none of it.
     const int t_lo = (int)max((int64_t)-1, 1 - ia);
     const int t_hi = (int)min((int64_t)(n + 2), g.H - ia + 1);
+    // planes t < tf are fetched (the window holds planes ia-2 .. ib-1 only)
+    const int tf = min(n + 1, t_hi);
     const bool okx = kk >= 0 && kk < (int)g.D, oky = kk + 1 >= 0 && kk + 1 < (int)g.D;
     const uint32_t lanekeep = (okx ? 0x0000FFFFu : 0u) | (oky ? 0xFFFF0000u : 0u);
     const int kc = EDGE == 0 ? kk : VEC ? min(max(kk, 0), (int)g.D - 2) : min(max(kk, 0), (int)g.D - 1);
@@ -211,7 +213,7 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
     const T* ptr = buf + ((ia - 2 - g.first) * pe + (int64_t)(j0 - 1) * Di + kc);
 
     auto fetch = [&](int t, const T* at, P2(&dst)[NR]) {
-        if (t >= t_lo && t < t_hi) {
+        if (t >= t_lo && t < tf) {
             if constexpr (EDGE == 2) {
 #pragma unroll
                 for (int r = 0; r < NR; ++r)
@@ -371,7 +373,6 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
     // field's last chunk (plane H) can follow, with a sentinel plane
     uint32_t V[NR];
     const int nm = min(n, t_hi - 1);
-    const int tf = min(n + 1, t_hi);  // planes t < tf are fetched
     int s = 0;
     for (; s < nm; s += 2) {
         quant_in(ra, V);  // plane t = s+1

@@ -172,6 +172,22 @@ def lattice_ok(ndim, shape, M, x=None):
     return (M + 1) * 4 <= 0xFFFF
 
 
+_row_w_cache = {}
+
+
+def _row_weights(row_w, dev):
+    """Row weights on ``dev``, uploaded once per (table, device): a pageable
+    H2D copy per call would block the host until the stream drains and leave
+    the GPU idle between back-to-back launches."""
+    a = np.ascontiguousarray(np.asarray(row_w, np.int64))
+    key = (a.shape, a.tobytes(), str(dev))
+    w = _row_w_cache.get(key)
+    if w is None:
+        w = torch().from_numpy(a.copy()).to(dev)
+        _row_w_cache[key] = w
+    return w
+
+
 def curves_from_rows(hist, M, row_w):
     """Device weighted prefix scan of histogram rows -> int64 numerators
     [n_desc, M+1] (or [batch, n_desc, M+1])."""
@@ -180,7 +196,7 @@ def curves_from_rows(hist, M, row_w):
     dev = hist.device
     batch = hist.shape[0] if hist.dim() == 3 else 1
     n_rows = hist.shape[-2]
-    w = t.from_numpy(np.ascontiguousarray(np.asarray(row_w, np.int64))).to(dev)
+    w = _row_weights(row_w, dev)
     n_desc = w.shape[0]
     out = t.empty((n_desc, M + 1) if batch == 1 else (batch, n_desc, M + 1), dtype=t.int64, device=dev)
     rc = L.ft_curves(ctypes.c_void_p(hist.data_ptr()), n_rows, M, batch, n_desc, ctypes.c_void_p(w.data_ptr()),

@@ -115,3 +115,16 @@ def test_lines_column_tiles(ft, orc, D):
     got = ft.descriptor_curves(src, _tabs(ft), path="lines")
     for c, w in zip(got, _want(orc, ft, x, 511, (0.0, 1.0))):
         assert np.array_equal(c.numerators, w)
+
+
+def test_lines_streaming_short_segments(ft, orc):
+    """Pinned streaming in windows of a few planes over a field wide enough
+    that the even CTA split cuts the windows into segments of one or two
+    planes: the march must not read past a window's last plane."""
+    import torch
+    x = _grf((23, 200, 190), 2.0, 91)
+    want = _want(orc, ft, x, 511, (0.0, 1.0))
+    for planes in (3, 4, 7):
+        got = ft.descriptor_curves(ft.ArraySource(x, 511, value_range=(0.0, 1.0)), _tabs(ft),
+                                   chunk_bytes=planes * 200 * 190 * 4)
+        assert all(np.array_equal(c.numerators, w) for c, w in zip(got, want)), planes

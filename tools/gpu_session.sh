@@ -14,7 +14,7 @@ timeout 1500 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.json 2> gp
 timeout 1500 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"lines|lattice|hist3d|curve_kernel|qmap" --csv \
     --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:lines3d -s 2 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:lines3d -s 1 -c 1 \
     -o /tmp/ncu/prof_main -f python tools/prof_run.py c5 2 lines > gpurun_out/ncu_main.log 2>&1
 ncu -i /tmp/ncu/prof_main.ncu-rep --page raw --csv > gpurun_out/prof_main_raw.csv 2>&1
 ncu -i /tmp/ncu/prof_main.ncu-rep --page details --csv > gpurun_out/prof_main_details.csv 2>&1
