@@ -399,26 +399,35 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
 }
 
 // The CTA tiles (TJ = 16 R rows x 62 columns) of ntk column tiles, rows up to
-// the last tile holding an interior strip, times the planes, as ONE linear
-// range cut evenly over the CTAs: every CTA marches the same number of
-// tile-planes (segments of consecutive planes of one tile), so no CTA waits
-// on a quantised item count.  Warp strips with rows outside 1 .. W-1 are left
-// to the warp loop.  f(j0, column tile, ia, ib).
+// the last tile holding an interior strip, times the planes.  Full rounds:
+// CTA b marches tile r G + b over every plane (the G CTAs of a round hold
+// adjacent tiles at about the same planes, so the halo rows and the partial
+// 32-byte sectors at tile edges are read from DRAM once and hit L2 for the
+// neighbour).  The leftover tiles x planes are cut evenly over the CTAs
+// (tile-major segments of consecutive planes), so no CTA waits on a quantised
+// item count.  Warp strips with rows outside 1 .. W-1 are left to the warp
+// loop.  f(j0, column tile, ia, ib).
 template <int R, typename F>
 __device__ __forceinline__ void cta_tiles(const LGeo& g, int ntk, int64_t np, int warp, F&& f)
 {
     constexpr int TJ = (LINES_NTH / 32) * R;
-    const int64_t T = (int64_t)g.tiles_j * ntk * np;
-    const int64_t u_end = T * (blockIdx.x + 1) / gridDim.x;
-    for (int64_t u = T * blockIdx.x / gridDim.x; u < u_end;) {
-        const int tile = (int)(u / np);
-        const int64_t p = u - (int64_t)tile * np;
-        const int64_t seg = min(u_end - u, np - p);
-        u += seg;
+    const int G = gridDim.x, b = blockIdx.x;
+    const int ntiles = g.tiles_j * ntk;
+    const int rounds = ntiles / G;
+    auto seg = [&](int tile, int64_t p0, int64_t p1) {
         const int tj = tile / ntk;
         const int j0 = tj * TJ + warp * R;
-        if (!(j0 >= 1 && j0 + R < g.W)) continue;  // the warp loop's
-        f(j0, tile - tj * ntk, g.v0 + p, g.v0 + p + seg);
+        if (j0 >= 1 && j0 + R < g.W) f(j0, tile - tj * ntk, g.v0 + p0, g.v0 + p1);
+    };
+    for (int r = 0; r < rounds; ++r) seg(r * G + b, 0, np);
+    const int64_t T = (int64_t)(ntiles - rounds * G) * np;
+    const int64_t u_end = T * (b + 1) / G;
+    for (int64_t u = T * b / G; u < u_end;) {
+        const int t = (int)(u / np);
+        const int64_t p = u - (int64_t)t * np;
+        const int64_t len = min(u_end - u, np - p);
+        u += len;
+        seg(rounds * G + t, p, p + len);
     }
 }
 
