@@ -127,6 +127,19 @@ int ft_lines3d(const ft_window *win, int64_t H, int64_t W, int64_t D, int64_t v0
                const ft_quant *q, int32_t M, uint64_t *hist, void *stream);
 int ft_lines3d_ok(int32_t M);
 
+/* Fused curve path for 2D EC_8C / perimeter / area (ft_lines2d.cu), batched
+ * like ft_lattice2d: the same rows 0..2 (cells, edge mins, vertex mins) of
+ * hist [batch][4][M+2], accumulated, computed with the vertices from sparse
+ * 1D extremum events (EC = sum over column lines of chi1(min over adjacent
+ * columns) - chi1(column)); row 3 (vertex maxes, EC_4C) is not
+ * touched -- use ft_lattice2d with maxes for it.  Replaces the same
+ * reference path as ft_lattice2d (contrib2d.py:161-232 + descriptors.py:
+ * 169-178).  Window: rows v0-2 .. v1-1.  Requires ft_lines2d_ok(M)
+ * (M <= ~1000). */
+int ft_lines2d(const ft_window *win, int64_t H, int64_t W, int64_t v0, int64_t v1,
+               const ft_quant *q, int32_t M, uint64_t *hist, void *stream);
+int ft_lines2d_ok(int32_t M);
+
 /* Transition histograms -> contribution maps and descriptor curves.
  * hist [batch][C][M+2] (C = 6 or 40).  q_in / q_out (may be NULL): device
  * uint64 [batch][T][M+2], OVERWRITTEN with the reference maps

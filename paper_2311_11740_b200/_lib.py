@@ -17,7 +17,7 @@ FT_I32, FT_U8, FT_U16, FT_F32, FT_F64 = 0, 1, 2, 3, 4
 FT_Q_IDENTITY, FT_Q_TABLE, FT_Q_TABLE_ROBUST, FT_Q_POW2 = 0, 1, 2, 3
 FT_ERR_ARG, FT_ERR_CLASSIFY, FT_ERR_CUDA_BASE = 1, 2, 1000
 
-EXPORTS = ("ft_hist2d", "ft_hist3d", "ft_lattice2d", "ft_lattice3d", "ft_lines3d", "ft_lines3d_ok", "ft_finalize", "ft_curves", "ft_class_weights", "ft_tables",
+EXPORTS = ("ft_hist2d", "ft_hist3d", "ft_lattice2d", "ft_lattice3d", "ft_lines3d", "ft_lines3d_ok", "ft_lines2d", "ft_lines2d_ok", "ft_finalize", "ft_curves", "ft_class_weights", "ft_tables",
            "ft_quantize", "ft_minmax", "ft_key_to_double", "ft_key64_to_double", "ft_version")
 
 
@@ -64,6 +64,8 @@ def load(build_if_missing=True):
         L.ft_lattice2d.argtypes = [P(ft_window), i64, i64, i64, i64, P(ft_quant), i32, i32, vp, vp]
         L.ft_lines3d.argtypes = [P(ft_window), i64, i64, i64, i64, i64, P(ft_quant), i32, vp, vp]
         L.ft_lines3d_ok.argtypes = [i32]
+        L.ft_lines2d.argtypes = [P(ft_window), i64, i64, i64, i64, P(ft_quant), i32, vp, vp]
+        L.ft_lines2d_ok.argtypes = [i32]
         L.ft_finalize.argtypes = [i32, i32, i64, vp, vp, vp, i32, vp, vp, vp]
         L.ft_curves.argtypes = [vp, i32, i32, i64, i32, vp, vp, vp]
         L.ft_class_weights.argtypes = [i32, vp, vp]

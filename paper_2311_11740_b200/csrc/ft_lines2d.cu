@@ -1,0 +1,328 @@
+// ft_lines2d.cu -- fused EC (8C) / perimeter / area histograms of 2D fields
+// and batches of them by line decomposition: the 2D counterpart of
+// ft_lines.cu.
+//
+// The reference builds the 2D curves from per-vertex transition counts
+// (contrib2d.py:161-232) folded with the weight tables (descriptors.py:
+// 169-178).  ft_lattice.cu restates them as element counts by level
+// (EC_8C = V - E + C, perimeter = 2E - 4C, area = C) with one dense vertex
+// event per lattice point.  Here the vertices come from sparse events:
+//
+// * Slicing the closed pixel complex along the lattice lines between columns
+//   (the closed line x = j, j = 0..W, and the open strips between them,
+//   chi_c(open strip) = -chi of its column) gives
+//       chi_2D = sum over i-lines of chi1(B) - chi1(A),
+//   A = cell levels of a column, B = min over columns (j-1, j), both on the
+//   lattice columns j in [0, W] (sentinel cells outside).  A line of unit
+//   intervals has chi1 = sum of +1 (local minimum along i) / -1 (local
+//   maximum), ties lower-i-first: ~10 % of the cells of a smooth field.
+// * Cells and edges are booked once per cell by signature: row u + 5 (s + 1),
+//   u = #edge neighbours activating first under the (level, index) order (so
+//   E = sum (4 - u)), s = the cell's own A-line event.
+//
+// Per 64 cells: 2 dense ATOMS (signature) + 2 sparse (B events), against 4
+// dense for lattice2d_rb_kernel.  Output rows per image (uint64 [4][M+2],
+// accumulated, the lattice2d layout): C, E, V = EC + E - C; row 3 (vertex
+// maxes, EC_4C) is left to ft_lattice2d.
+#include "ft_lines.cuh"
+
+namespace ft {
+
+constexpr int L2L_NTH = 512;  // 16 warps, each a 62-column strip
+constexpr int L2L_RB = 64;    // rows per (row block, column tile) piece
+constexpr int L2L_SIG = 15;   // signature rows u + 5 (s + 1)
+
+// One warp strip: lattice columns k0 .. k0+61 of one image, lattice rows
+// [ia, ib).  Lane l holds cells (kk, kk+1), kk = k0-1+2l; lane 0 computes its
+// high half, lane 31 its low half (as in ft_lines.cu).  EDGE: columns outside
+// the image (clamped pair loads, masked halves).
+template <int DT, int QM, bool VEC, bool EDGE>
+__device__ __forceinline__ void lines2d_item(const typename Elem<DT>::T* __restrict__ img, const LGeo& g,
+                                             const QuantDev& q, const float* __restrict__ tt, int64_t ia,
+                                             int64_t ib, int k0, int lane)
+{
+    using P2 = typename Pair<DT>::T;
+    using T = typename Elem<DT>::T;
+    constexpr uint32_t FULL = 0xFFFFFFFFu;
+    const int Wi = (int)g.W;
+    const uint32_t sent4 = (uint32_t)(g.M + 1) * 4u;
+    const uint32_t S2 = sent4 * 0x10001u + LINES_SB2;
+    const uint32_t hk = (uint32_t)g.hk;
+    const uint32_t ONE = g.one, MONE = 0u - g.one;
+    const float Mf = (float)g.M;
+    const int kk = k0 - 1 + 2 * lane;
+    const uint32_t lmask = __shfl_sync(FULL, lane == 0 ? 0xFFFF0000u : lane == 31 ? 0x0000FFFFu : FULL, lane);
+    const uint32_t dummy2 = S2;
+    const int n = (int)(ib - ia);
+    // rows t = -1 .. n (row ia-1+t) exist iff t_lo <= t < t_hi; rows t < tf
+    // are fetched (a window holds rows ia-2 .. ib-1)
+    const int t_lo = (int)max((int64_t)-1, 1 - ia);
+    const int t_hi = (int)min((int64_t)(n + 2), g.H - ia + 1);
+    const int tf = min(n + 1, t_hi);
+    const bool okx = kk >= 0 && kk < Wi, oky = kk + 1 >= 0 && kk + 1 < Wi;
+    const uint32_t lanekeep = (okx ? 0x0000FFFFu : 0u) | (oky ? 0xFFFF0000u : 0u);
+    const int kc = !EDGE ? kk : VEC ? min(max(kk, 0), Wi - 2) : min(max(kk, 0), Wi - 1);
+    const T* ptr = img + ((ia - 2 - g.first) * g.W + kc);  // row ia-2 (t = -1)
+
+    auto fetch = [&](int t, const T* at, P2& dst) {
+        if (t >= t_lo && t < tf) dst = load_pair<DT, VEC>(at, true, EDGE ? kk + 1 < Wi : true);
+    };
+    auto quant_in = [&](const P2& src) -> uint32_t {
+        uint32_t v;
+        if constexpr (QM == FT_Q_POW2)
+            v = pack_pow2_sat<DT>(src, q.inv, Mf, g.four);
+        else
+            v = pack_pair<DT, QM, 0>(src, true, true, tt, q, g.M, sent4) + LINES_SB2;
+        return EDGE ? sel_mask(lanekeep, v, S2) : v;
+    };
+    auto quant = [&](int t, const P2& src) -> uint32_t { return t >= t_lo && t < t_hi ? quant_in(src) : S2; };
+
+    struct St {
+        uint32_t pV, tmi, pWm, pC, eC;
+    };
+    St sa, sb;
+    P2 raw[4];  // rows in flight: raw[p] holds row t = p+1 (mod 4)
+    {
+        P2 r0, r1;
+        fetch(-1, ptr, r0);
+        fetch(0, ptr + g.W, r1);
+        const uint32_t V0 = quant(-1, r0);
+        sa.pV = quant(0, r1);
+        const uint32_t Wm0 = shift_pair(__shfl_up_sync(FULL, V0, 1), V0);
+        sa.pWm = shift_pair(__shfl_up_sync(FULL, sa.pV, 1), sa.pV);
+        const uint32_t C0 = vmin2(V0, Wm0);
+        sa.pC = vmin2(sa.pV, sa.pWm);
+        sa.tmi = hff(cmp2(V0, sa.pV));  // the -i neighbour (row ia-2) activates first
+        sa.eC = cmp2(C0, sa.pC);
+    }
+#pragma unroll
+    for (int p = 0; p < 4; ++p) fetch(p + 1, ptr + (p + 2) * g.W, raw[p]);
+    ptr += 6 * g.W;  // row t = 5
+
+    // row t arrives in V; every event of the row before it (state o) is booked
+    auto step = [&](uint32_t V, const St& o, St& x) {
+        const uint32_t Wm = shift_pair(__shfl_up_sync(FULL, V, 1), V);
+        const uint32_t Cn = vmin2(V, Wm);
+        const uint32_t cb = o.pV | 0x80008000u;
+        const uint32_t cb1 = cb * ONE + 0xFFFEFFFFu;  // cb - 0x10001
+        const uint32_t t2 = hff(o.pWm * MONE + cb);   // -j neighbour first
+        const uint32_t t3 = hff(V * MONE + cb1);      // +i neighbour first
+        // +j: complement of the right neighbour's -j term
+        const uint32_t t5 = shift_pair(t2, __shfl_down_sync(FULL, t2, 1)) * MONE + FF2;
+        // row u + 5 (s + 1) = t2 + t5 + 10 - 4 (tmi + t3), units of 255, >= 2
+        uint32_t sum = t2 * ONE + 10u * FF2;
+        sum = t5 * ONE + sum;
+        const uint32_t row = (o.tmi * ONE + t3) * (uint32_t)(-4) + sum;
+        sinc2<0>(sel_mask(lmask, row * hk + o.pV, dummy2));
+        // B line (min over columns j-1, j): +1 at a local min (plus row), -1
+        // at a local max (minus row)
+        const uint32_t nC = cmp2(o.pC, Cn);
+        sinc2<LINES_PLUS>(ev_sel((o.eC ^ nC) & lmask, o.pC | (~nC & 0x80008000u), dummy2));
+        x.tmi = t3 * MONE + FF2;
+        x.pWm = Wm;
+        x.pC = Cn;
+        x.eC = nC;
+        x.pV = V;
+    };
+
+    // steps s < nm see an existing row t = s+1; only the last step of the
+    // image's last segment (row H) can follow, with a sentinel row
+    const int nm = min(n, t_hi - 1);
+    int s = 0;
+    // steady state: 4 steps per iteration, every refill (rows s+5 .. s+8)
+    // inside the segment -- no guards
+    for (; s + 4 <= nm && s + 8 < tf; s += 4) {
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            const uint32_t V = quant_in(raw[p]);
+            raw[p] = load_pair<DT, VEC>(ptr + p * g.W, true, EDGE ? kk + 1 < Wi : true);
+            if (p & 1)
+                step(V, sb, sa);
+            else
+                step(V, sa, sb);
+        }
+        ptr += 4 * g.W;
+    }
+    for (; s < nm; s += 4) {
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            if (s + p < nm) {
+                const uint32_t V = quant_in(raw[p]);
+                fetch(s + p + 5, ptr + p * g.W, raw[p]);
+                if (p & 1)
+                    step(V, sb, sa);
+                else
+                    step(V, sa, sb);
+            }
+        }
+        ptr += 4 * g.W;
+    }
+    if (nm < n) {  // at most one step: the absent row H
+        if (nm & 1)
+            step(S2, sb, sa);
+        else
+            step(S2, sa, sb);
+    }
+}
+
+// Work: per image, lattice rows [v0, v1) in row blocks of L2L_RB, x column
+// tiles; unit = one (tile, row) and the order (row block, tile, row), so the
+// warps of a CTA hold adjacent tiles of the same rows.  All images' units
+// form one range cut evenly over the CTAs; inside a CTA each image's share is
+// cut evenly over the 16 warps, then the CTA folds that image's bins into
+// hist[image] (one __syncthreads pair per image).
+template <int DT, int QM, bool VEC>
+__global__ void __launch_bounds__(L2L_NTH, 2) lines2d_kernel(const typename Elem<DT>::T* __restrict__ buf, LGeo g,
+                                                             QuantDev q, unsigned long long* __restrict__ hist)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    char* h = reinterpret_cast<char*>(smem_raw);
+    const int M2 = g.M + 2;
+    const int hs = g.hs;
+    const int end = LINES_PLUS + LINES_MINUS + hs;
+    float* tt = reinterpret_cast<float*>(h + LINES_PLUS + hs);
+    uint32_t* hw = reinterpret_cast<uint32_t*>(h);
+    for (int i = threadIdx.x; i < end / 4; i += blockDim.x) hw[i] = 0;
+    __syncthreads();
+    if (QM != FT_Q_IDENTITY && QM != FT_Q_POW2)
+        for (int i = threadIdx.x; i < M2; i += blockDim.x) tt[i] = q.tt[i];
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NW = L2L_NTH / 32;
+    const int64_t nrows = g.v1 - g.v0;
+    const int ntiles = g.tiles_k;
+    const int64_t Timg = cdiv(nrows, (int64_t)L2L_RB) * ntiles * L2L_RB;
+    const int64_t batch = g.n_items;  // images
+    const int64_t total = batch * Timg;
+    const int64_t U0 = total * blockIdx.x / gridDim.x, U1 = total * (blockIdx.x + 1) / gridDim.x;
+    const int rw = hs / 4, pm = LINES_PLUS / 4;
+    for (int64_t b = U0 / Timg; b < batch && b * Timg < U1; ++b) {
+        const int64_t a = max(U0, b * Timg) - b * Timg, e = min(U1, (b + 1) * Timg) - b * Timg;
+        const int64_t wa = a + (e - a) * warp / NW, we = a + (e - a) * (warp + 1) / NW;
+        const typename Elem<DT>::T* img = buf + b * g.bstride;
+        for (int64_t u = wa; u < we;) {
+            const int64_t piece = u / L2L_RB;
+            const int r = (int)(u - piece * L2L_RB);
+            const int64_t len = min(we - u, (int64_t)(L2L_RB - r));
+            u += len;
+            const int64_t rb = piece / ntiles;
+            const int t = (int)(piece - rb * ntiles);
+            const int64_t r0 = rb * L2L_RB + r, r1 = min(r0 + len, nrows);
+            if (r0 >= r1) continue;
+            const int k0 = t * 62 - 1;
+            if (k0 >= 1 && k0 + 63 <= g.W)
+                lines2d_item<DT, QM, VEC, false>(img, g, q, tt, g.v0 + r0, g.v0 + r1, k0, lane);
+            else
+                lines2d_item<DT, QM, VEC, true>(img, g, q, tt, g.v0 + r0, g.v0 + r1, k0, lane);
+        }
+        __syncthreads();
+        // fold: C = sum of signature rows, E = sum (4 - u) rows, EC = plus -
+        // minus - sum s rows, V = EC + E - C
+        unsigned long long* out = hist + b * 4 * M2;
+        for (int l = threadIdx.x; l < M2; l += blockDim.x) {
+            uint32_t c = 0, ed = 0;
+            int32_t ec = (int32_t)(hw[pm + l] - hw[pm + LINES_MINUS / 4 + l]);
+            hw[pm + l] = 0;
+            hw[pm + LINES_MINUS / 4 + l] = 0;
+#pragma unroll
+            for (int s = 0; s < L2L_SIG; ++s) {
+                const uint32_t v = hw[s * rw + l];
+                hw[s * rw + l] = 0;
+                c += v;
+                ed += (uint32_t)(4 - s % 5) * v;
+                ec -= (s / 5 - 1) * (int32_t)v;
+            }
+            const int64_t vx = (int64_t)ec + (int64_t)ed - (int64_t)c;
+            if (c) atomicAdd(&out[l], (unsigned long long)c);
+            if (ed) atomicAdd(&out[M2 + l], (unsigned long long)ed);
+            if (vx) atomicAdd(&out[2 * M2 + l], (unsigned long long)vx);
+        }
+        __syncthreads();
+    }
+}
+
+// 16-bit packed signature offsets: 14 hs + (M + 1) * 4 + base must fit
+static int lines2d_hs(int M) { return 255 * (int)cdiv(cdiv((int64_t)(M + 2) * 4, 255), 4) * 4; }
+static bool lines2d_ok(int M)
+{
+    const int hs = lines2d_hs(M);
+    return (M + 2) * 4 <= hs && (L2L_SIG - 1) * hs + (M + 1) * 4 + (int)LINES_SBASE < LINES_PLUS &&
+           (M + 1) * 4 + (int)LINES_SBASE < LINES_MINUS && hs + (M + 2) * 4 <= LINES_MINUS;
+}
+
+template <int DT, int QM>
+static int launch_lines2d(const ft_window* win, int64_t H, int64_t W, int64_t v0, int64_t v1, const ft_quant* qa,
+                          int32_t M, uint64_t* hist, cudaStream_t st)
+{
+    using T = typename Elem<DT>::T;
+    LGeo g{};
+    g.H = H; g.W = W; g.D = 1; g.v0 = v0; g.v1 = v1; g.first = win->first; g.M = M;
+    g.bstride = win->batch_stride;
+    g.hs = lines2d_hs(M);
+    g.hk = g.hs / 255;
+    g.one = 1;
+    g.four = 4;
+    g.tiles_k = (int)((W + 1) / 62 + 1);  // tile t: lattice columns 62 t - 1 .. 62 t + 60
+    g.n_items = std::max<int64_t>(win->batch, 1);
+    const bool vec = W % 2 == 0 && (g.n_items <= 1 || win->batch_stride % 2 == 0) &&
+                     reinterpret_cast<uintptr_t>(win->data) % (2 * sizeof(T)) == 0;
+    if (const int rc = lines_check_sbase()) return rc;
+    QuantDev qd = qdev(qa);
+    if (QM == FT_Q_POW2) qd.inv = M > 0 ? qd.scale / (float)M : 0.f;
+    const size_t smem = (size_t)(LINES_PLUS + LINES_MINUS + g.hs);
+    auto kern = vec ? lines2d_kernel<DT, QM, true> : lines2d_kernel<DT, QM, false>;
+    FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    FT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L2L_NTH, smem));
+    if (per_sm < 1) return FT_ERR_ARG;
+    const int64_t units = g.n_items * cdiv(v1 - v0, (int64_t)L2L_RB) * g.tiles_k * L2L_RB;
+    // >= 16 * 64 units (one piece per warp) per CTA
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm_l() * per_sm,
+                                                                cdiv(units, (int64_t)(L2L_NTH / 32) * L2L_RB)));
+    kern<<<(int)grid, L2L_NTH, smem, st>>>(static_cast<const T*>(win->data), g, qd,
+                                          reinterpret_cast<unsigned long long*>(hist));
+    FT_CUDA_TRY(cudaGetLastError());
+    return FT_OK;
+}
+
+}  // namespace ft
+
+#ifndef FT_DEV_KERNEL_ONLY
+using namespace ft;
+
+extern "C" int ft_lines2d(const ft_window* win, int64_t H, int64_t W, int64_t v0, int64_t v1, const ft_quant* q,
+                          int32_t M, uint64_t* hist, void* stream)
+{
+    if (!win || !hist || H < 1 || W < 1 || M < 0 || v0 < 0 || v1 > H + 1 || v0 > v1) return FT_ERR_ARG;
+    if (!lines2d_ok(M)) return FT_ERR_ARG;
+    if (win->batch > 1 && win->batch_stride < win->count * W) return FT_ERR_ARG;
+    if (v0 == v1) return FT_OK;
+    if (!window_ok(win, H, v0, v1, 2)) return FT_ERR_ARG;
+    const int qm = effective_qmode(q, true);
+    if (qm != FT_Q_IDENTITY && !q->thresholds) return FT_ERR_ARG;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    switch (win->dtype) {
+    case FT_I32:
+        if (qm != FT_Q_IDENTITY) return FT_ERR_ARG;
+        return launch_lines2d<FT_I32, FT_Q_IDENTITY>(win, H, W, v0, v1, q, M, hist, st);
+    case FT_U8:
+        if (qm == FT_Q_IDENTITY) return launch_lines2d<FT_U8, FT_Q_IDENTITY>(win, H, W, v0, v1, q, M, hist, st);
+        if (qm == FT_Q_TABLE || qm == FT_Q_POW2) return launch_lines2d<FT_U8, FT_Q_TABLE>(win, H, W, v0, v1, q, M, hist, st);
+        return launch_lines2d<FT_U8, FT_Q_TABLE_ROBUST>(win, H, W, v0, v1, q, M, hist, st);
+    case FT_U16:
+        if (qm == FT_Q_IDENTITY) return launch_lines2d<FT_U16, FT_Q_IDENTITY>(win, H, W, v0, v1, q, M, hist, st);
+        if (qm == FT_Q_POW2) return launch_lines2d<FT_U16, FT_Q_POW2>(win, H, W, v0, v1, q, M, hist, st);
+        if (qm == FT_Q_TABLE) return launch_lines2d<FT_U16, FT_Q_TABLE>(win, H, W, v0, v1, q, M, hist, st);
+        return launch_lines2d<FT_U16, FT_Q_TABLE_ROBUST>(win, H, W, v0, v1, q, M, hist, st);
+    case FT_F32:
+        if (qm == FT_Q_IDENTITY) return FT_ERR_ARG;
+        if (qm == FT_Q_POW2) return launch_lines2d<FT_F32, FT_Q_POW2>(win, H, W, v0, v1, q, M, hist, st);
+        if (qm == FT_Q_TABLE) return launch_lines2d<FT_F32, FT_Q_TABLE>(win, H, W, v0, v1, q, M, hist, st);
+        return launch_lines2d<FT_F32, FT_Q_TABLE_ROBUST>(win, H, W, v0, v1, q, M, hist, st);
+    }
+    return FT_ERR_ARG;
+}
+
+extern "C" int ft_lines2d_ok(int32_t M) { return M >= 0 && lines2d_ok(M) ? 1 : 0; }
+#endif  // FT_DEV_KERNEL_ONLY

@@ -9,6 +9,7 @@ treats as uint64 (counts never exceed 2**63).
 from __future__ import annotations
 
 import ctypes
+import os as _os
 
 import numpy as np
 
@@ -113,10 +114,23 @@ def new_lattice_hist(ndim, M, device, batch=1):
     return torch().zeros(shape, dtype=torch().int64, device=device)
 
 
+def _use_lines2d(kernel, batch):
+    """ft_lines2d or ft_lattice2d for 2D rows 0..2.  Measured on B200
+    (profiles/r01/lines2d_notes.md): the line kernel wins on batches of
+    images (C3: 739 vs 682 Gpix/s), the lattice kernel on one large image
+    (C2: 548 vs 486).  ``kernel`` "lines" / "lattice" (or FT_2D_KERNEL)
+    forces one."""
+    force = kernel if kernel != "auto" else _os.environ.get("FT_2D_KERNEL", "auto")
+    if force in ("lines", "lattice"):
+        return force == "lines"
+    return batch > 1
+
+
 def launch_lattice(ndim, x, shape, M, quant, rows=None, first=0, hist=None, batch=1, batch_stride=0,
-                   maxes=False):
+                   maxes=False, kernel="auto"):
     """Accumulate the fused-curve element histograms (ft_lattice2d/3d) of
-    lattice rows ``rows`` = [v0, v1); arguments as ``launch_hist``."""
+    lattice rows ``rows`` = [v0, v1); arguments as ``launch_hist``.  2D
+    without vertex maxes may go to ft_lines2d (same rows, _use_lines2d)."""
     L = _lib.load()
     dev = x.device
     H = shape[0]
@@ -128,6 +142,13 @@ def launch_lattice(ndim, x, shape, M, quant, rows=None, first=0, hist=None, batc
                          int(batch), int(batch_stride))
     qs, keep = device_struct(quant, dev)
     st = _stream_ptr(dev)
+    if ndim == 2 and not maxes and lines2d_ok(M) and _use_lines2d(kernel, batch):
+        # rows 0..2 by line decomposition (ft_lines2d): fewer shared atomics
+        rc = L.ft_lines2d(ctypes.byref(win), H, shape[1], v0, v1, ctypes.byref(qs), M,
+                          ctypes.c_void_p(hist.data_ptr()), st)
+        del keep
+        _lib.check(rc, "ft_lines2d")
+        return hist
     if ndim == 2:
         rc = L.ft_lattice2d(ctypes.byref(win), H, shape[1], v0, v1, ctypes.byref(qs), M, int(maxes),
                             ctypes.c_void_p(hist.data_ptr()), st)
@@ -159,6 +180,11 @@ def launch_lines(x, shape, M, quant, rows=None, first=0, hist=None):
     del keep
     _lib.check(rc, "ft_lines3d")
     return hist
+
+
+def lines2d_ok(M):
+    """Whether ft_lines2d takes this level count."""
+    return bool(_lib.load().ft_lines2d_ok(int(M)))
 
 
 def lines_ok(M):

@@ -108,3 +108,48 @@ def test_lines_level_limit():
     L = _lib.load()
     assert L.ft_lines3d_ok(511) == 1 and L.ft_lines3d_ok(1023) == 1 and L.ft_lines3d_ok(2000) == 1
     assert L.ft_lines3d_ok(4000) == 0 and L.ft_lines3d_ok(-1) == 0
+
+
+# ---- 2D (csrc/ft_lines2d.cu) -------------------------------------------------
+
+def lines2d_rows(levels, M):
+    """(C, E, V) rows by level as ft_lines2d accumulates them: signature rows
+    (u = #edge neighbours first, s = the cell's own column-line event) and
+    the events of the lines B_j = min over columns (j-1, j), j in [0, W];
+    EC_8C = sum chi1(B) - sum chi1(A) (slicing along the lines between
+    columns), V = EC + E - C."""
+    lv = np.asarray(levels, np.int64)
+    H, W = lv.shape
+    p = np.pad(lv, 1, constant_values=M + 1)
+    q = p[1:H + 1]
+    A = q[:, 1:W + 2]  # lattice columns j in [0, W]
+    B = np.minimum(q[:, 0:W + 1], A)
+    ec = _line_events(B, M) - _line_events(A, M)
+    c = p[1:-1, 1:-1]
+    u = np.zeros_like(c)
+    for ax in range(2):
+        lo = [slice(1, -1)] * 2
+        hi = [slice(1, -1)] * 2
+        lo[ax] = slice(0, -2)
+        hi[ax] = slice(2, None)
+        u += (p[tuple(lo)] <= c).astype(np.int64) + (p[tuple(hi)] < c).astype(np.int64)
+    cells = _hist(c, M)
+    edges = _hist(c, M, 4 - u)
+    return cells, edges, ec + edges - cells
+
+
+def test_model2d_matches_reference_golden_curves(golden):
+    for n in range(int(golden["n_f2d"])):
+        lv, M = golden[f"f2d{n}_levels"], int(golden[f"f2d{n}_M"])
+        cells, edges, verts = lines2d_rows(lv, M)
+        want = golden[f"f2d{n}_curves"]  # ec 8C, ec 4C, perimeter, area
+        assert np.array_equal(np.cumsum(verts - edges + cells)[:M + 1] * 8, want[0]), n
+        assert np.array_equal(np.cumsum(2 * edges - 4 * cells)[:M + 1] * 8, want[2]), n
+        assert np.array_equal(np.cumsum(cells)[:M + 1] * 8, want[3]), n
+
+
+def test_lines2d_level_limit():
+    from paper_2311_11740_b200 import _lib
+    L = _lib.load()
+    assert L.ft_lines2d_ok(255) == 1 and L.ft_lines2d_ok(1000) == 1
+    assert L.ft_lines2d_ok(1100) == 0 and L.ft_lines2d_ok(-1) == 0
