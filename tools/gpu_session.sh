@@ -8,6 +8,7 @@ timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&
 timeout 300 python __graft_entry__.py > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout 600 python tools/prof_run.py c5 3 all > gpurun_out/prof_c5.log 2>&1
 timeout 600 python tools/prof_run.py c4a 3 all > gpurun_out/prof_c4a.log 2>&1
+timeout 600 python tools/prof_run.py c4b 3 all > gpurun_out/prof_c4b.log 2>&1
 timeout 600 python tools/prof_run.py c2 3 both > gpurun_out/prof_c2.log 2>&1
 timeout 900 python tools/prof_run.py c3 3 both > gpurun_out/prof_c3.log 2>&1
 timeout 1500 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err

@@ -1,6 +1,6 @@
 """Profiling driver: build a synthetic field on cuda:0 and launch the hot
 kernels a few times (for ncu / timing).
-    python tools/prof_run.py [c4a|c5|small|c2|c3] [reps] [map|lattice|lines|both|all]"""
+    python tools/prof_run.py [c4a|c4b|c5|small|c2|c3] [reps] [map|lattice|lines|both|all]"""
 import sys
 from pathlib import Path
 
@@ -22,6 +22,15 @@ if cfg in ("c4a", "c5", "small"):
     x = synth.grf_slab(shape, sigma, 2311, (0, shape[0]), dev)
     synth.normalise_(x, x.min(), x.max())
     q = ft.quant.QuantSpec.for_range(0.0, 1.0, M)
+elif cfg == "c4b":  # 1024 x 1024 x 256 u16 hyperspectral-like cube, auto-range quantize to 1024 levels
+    shape, M = (1024, 1024, 256), 1023
+    x = synth.grf_slab(shape, 3.0, 2311, (0, shape[0]), dev)
+    synth.normalise_(x, x.min(), x.max())
+    xi = torch.floor(x * 65535 + 0.5).to(torch.int32)
+    lo, hi = float(xi.min()), float(xi.max())
+    x = xi.to(torch.uint16)
+    del xi
+    q = ft.quant.QuantSpec.for_range(lo, hi, M)
 elif cfg == "c2":
     shape, M = (8192, 8192), 255
     x = synth.grf_2d(shape, 4.0, 2311, dev)
