@@ -1,7 +1,6 @@
 // Dev harness: instantiate ONE lines3d_kernel variant for fast ptxas / SASS checks.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include -Xptxas -v -cubin tools/dev/lines_one.cu
-#define FT_DEV_KERNEL_ONLY
-#include "../../paper_2311_11740_b200/csrc/ft_lines.cu"
+#include "../../paper_2311_11740_b200/csrc/ft_lines3d.cuh"
 #ifndef DEV_FOLD
 #define DEV_FOLD true
 #endif

@@ -1,5 +1,5 @@
-"""Build A/B variants of ft_lines.cu (F32 / FT_Q_POW2 path only) linked with the
-other objects of the main build:  python tools/dev/variants.py name="-DX=1 -DY=2" ...
+"""Build A/B variants of the benchmark path's translation unit (ft_lines_f32p.cu:
+f32 / FT_Q_POW2) linked with the other objects of the main build:  python tools/dev/variants.py name="-DX=1 -DY=2" ...
 Each lands in variants/<name>/libfieldtopo_b200.so (use with FT_LIB=...)."""
 import concurrent.futures as cf
 import subprocess
@@ -10,16 +10,16 @@ ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 from paper_2311_11740_b200 import build as b  # noqa: E402
 
-objs = [p for p in sorted(b.BUILD.glob("*.o")) if p.stem != "ft_lines"]
+objs = [p for p in sorted(b.BUILD.glob("*.o")) if p.stem != "ft_lines_f32p"]
 
 
 def one(spec):
     name, flags = spec.split("=", 1)
     out = ROOT / "variants" / name
     out.mkdir(parents=True, exist_ok=True)
-    obj = out / "ft_lines.o"
-    cmd = [b.nvcc(), *b.ARCH, *b.NVCC_FLAGS, "-DFT_LINES_F32_ONLY", *flags.split(), "-Xptxas", "-v", "-c",
-           str(b.CSRC / "ft_lines.cu"), "-o", str(obj)]
+    obj = out / "ft_lines_f32p.o"
+    cmd = [b.nvcc(), *b.ARCH, *b.NVCC_FLAGS, *flags.split(), "-Xptxas", "-v", "-c",
+           str(b.CSRC / "ft_lines_f32p.cu"), "-o", str(obj)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode:
         return f"{name}: FAILED\n{r.stderr[-2000:]}"
