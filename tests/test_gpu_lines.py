@@ -128,3 +128,21 @@ def test_lines_streaming_short_segments(ft, orc):
         got = ft.descriptor_curves(ft.ArraySource(x, 511, value_range=(0.0, 1.0)), _tabs(ft),
                                    chunk_bytes=planes * 200 * 190 * 4)
         assert all(np.array_equal(c.numerators, w) for c, w in zip(got, want)), planes
+
+
+def test_lines_raw_f32_streaming(ft, orc, tmp_path):
+    """Headerless float32 volume streamed from the file (RawVolumeSource
+    element "f32", the out-of-core entry point of SURVEY.md §8f row 3), with
+    an explicit range and with the streaming device min/max pass."""
+    from paper_2311_11740_b200.sources import RawVolumeSource
+    x = _grf((41, 70, 130), 2.0, 55)
+    x = (x * 3.0 - 1.0).astype(np.float32)  # range [-1, 2]: not a power-of-two span
+    p = tmp_path / "f.raw"
+    x.tofile(p)
+    for vr in ((-1.0, 2.0), None):
+        with RawVolumeSource(p, (70, 41, 130), "f32", 511, value_range=vr, chunk_bytes=1 << 20) as src:
+            want = _want(orc, ft, x, 511, src.value_range)
+            if vr is None:
+                assert src.value_range == (float(x.min()), float(x.max()))
+            got = ft.descriptor_curves(src, _tabs(ft), chunk_bytes=7 * 70 * 130 * 4)
+            assert all(np.array_equal(c.numerators, w) for c, w in zip(got, want)), vr
