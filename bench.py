@@ -266,6 +266,14 @@ def main():
     ms, kms = t_ms.tolist()
     cells = H * W * D
     value = cells / (ms / 1e3) / 1e9
+    # full-size parity properties (no oracle can run 2048^3 here): the curves
+    # of the benchmark kernel, of the independent drop-in map kernel on the
+    # same field, and (below) of the streamed end-to-end path must agree bit
+    # for bit; and the whole box (level M) is one contractible solid
+    resident = step().cpu().numpy() // plan[3][:, None]
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
     # the contribution-map kernel (drop-in gather_3d_*), same field, reported beside
     mhist = engine.new_hist(3, M, dev)
     map_ms = []
@@ -276,6 +284,11 @@ def main():
         k_end.record(stream)
         torch.cuda.synchronize()
         map_ms.append(k_start.elapsed_time(k_end))
+    if ws > 1:
+        import torch.distributed as dist
+        dist.all_reduce(mhist)
+    _, _, map_num = engine.finalize(3, M, mhist, maps=False, tables=eighths)
+    map_curves = map_num.cpu().numpy()
     del mhist
     map_gvox = (r1 - r0) * W * D / (statistics.median(map_ms) / 1e3) / 1e9
 
@@ -303,7 +316,7 @@ def main():
                                           kind=kind)
                 import torch.distributed as dist
                 dist.all_reduce(h)
-                curves = engine.curves_from_rows(h, M, row_w).cpu().numpy()
+                curves = engine.curves_from_rows(h, M, row_w).cpu().numpy() // plan[3][:, None]
             torch.cuda.synchronize()
             if it:
                 e_times.append(time.perf_counter() - s)
@@ -316,6 +329,11 @@ def main():
                "path": "descriptor_curves-equivalent: ArraySource over pinned host memory, 512 MiB chunks, "
                        "double-buffered H2D overlapped with the kernel, curves to host"}
         x = None
+    box = {"ec": 8, "surface-area": 8 * 2 * (H * W + W * D + H * D), "volume": 8 * H * W * D}
+    checks = {"map_kernel_curves_equal": bool(np.array_equal(map_curves, resident)),
+              "e2e_curves_equal": None if e2e is None else bool(np.array_equal(curves, resident)),
+              "full_box_at_level_M": bool(all(int(resident[i][M]) == box[d] for i, d in enumerate(descs))),
+              "volume_monotone": bool(np.all(np.diff(resident[list(descs).index("volume")]) >= 0))}
 
     # ---- CPU baseline (rank 0, N = 1 only) ----------------------------------
     cpu = None
@@ -336,7 +354,7 @@ def main():
                "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
                "scaling": "strong", "vs_baseline": None, "dtype": "f32 in, int32 levels, u64 histograms",
                "data": "synthetic (seeded device-generated GRF; no dataset in the reference)",
-               "config": config,
+               "config": config, "checks": checks,
                "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                             "frac": round(achieved / peak, 4),
                             "traffic": ncu_traffic() if plan[0] == "lines" and (H, W, D) == (2048, 2048, 2048) else None,
