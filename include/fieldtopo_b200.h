@@ -29,6 +29,7 @@ extern "C" {
 #define FT_OK 0
 #define FT_ERR_ARG 1
 #define FT_ERR_CLASSIFY 2
+#define FT_ERR_INTERNAL 3 /* unsupported device state (e.g. the shared-memory base the line kernels address absolutely) */
 #define FT_ERR_CUDA_BASE 1000
 
 /* element type of a field buffer */

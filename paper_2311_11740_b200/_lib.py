@@ -15,7 +15,7 @@ from ._tables import ClassificationError
 
 FT_I32, FT_U8, FT_U16, FT_F32, FT_F64 = 0, 1, 2, 3, 4
 FT_Q_IDENTITY, FT_Q_TABLE, FT_Q_TABLE_ROBUST, FT_Q_POW2 = 0, 1, 2, 3
-FT_ERR_ARG, FT_ERR_CLASSIFY, FT_ERR_CUDA_BASE = 1, 2, 1000
+FT_ERR_ARG, FT_ERR_CLASSIFY, FT_ERR_INTERNAL, FT_ERR_CUDA_BASE = 1, 2, 3, 1000
 
 EXPORTS = ("ft_hist2d", "ft_hist3d", "ft_lattice2d", "ft_lattice3d", "ft_lines3d", "ft_lines3d_ok", "ft_lines2d", "ft_lines2d_ok", "ft_finalize", "ft_curves", "ft_class_weights", "ft_tables",
            "ft_quantize", "ft_minmax", "ft_key_to_double", "ft_key64_to_double", "ft_version")
@@ -92,6 +92,8 @@ def check(rc, what=""):
         raise ValueError(f"{what}: invalid argument")
     if rc == FT_ERR_CLASSIFY:
         raise ClassificationError("3D neighborhood outside the configuration table")
+    if rc == FT_ERR_INTERNAL:
+        raise RuntimeError(f"{what}: unsupported device state (shared-memory layout)")
     if rc >= FT_ERR_CUDA_BASE:
         raise RuntimeError(f"{what}: CUDA error {rc - FT_ERR_CUDA_BASE}")
     raise RuntimeError(f"{what}: error code {rc}")

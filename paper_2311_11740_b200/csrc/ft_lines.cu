@@ -21,7 +21,7 @@ int lines_check_sbase()
     const cudaError_t e = cudaMemcpy(&v, d, 4, cudaMemcpyDeviceToHost);
     cudaFree(d);
     if (e != cudaSuccess) return FT_ERR_CUDA_BASE + (int)e;
-    state = v == LINES_SBASE ? FT_OK : FT_ERR_CLASSIFY;
+    state = v == LINES_SBASE ? FT_OK : FT_ERR_INTERNAL;
     return state;
 }
 
