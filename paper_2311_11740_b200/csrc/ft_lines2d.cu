@@ -36,7 +36,8 @@ constexpr int L2L_SIG = 15;   // signature rows u + 5 (s + 1)
 // [ia, ib).  Lane l holds cells (kk, kk+1), kk = k0-1+2l; lane 0 computes its
 // high half, lane 31 its low half (as in ft_lines.cu).  EDGE: columns outside
 // the image (clamped pair loads, masked halves).
-template <int DT, int QM, bool VEC, bool EDGE>
+// PF: rows in flight per lane (even: the ping-pong march state).
+template <int DT, int QM, bool VEC, bool EDGE, int PF>
 __device__ __forceinline__ void lines2d_item(const typename Elem<DT>::T* __restrict__ img, const LGeo& g,
                                              const QuantDev& q, const float* __restrict__ tt, int64_t ia,
                                              int64_t ib, int k0, int lane)
@@ -81,7 +82,7 @@ __device__ __forceinline__ void lines2d_item(const typename Elem<DT>::T* __restr
         uint32_t pV, tmi, pWm, pC, eC;
     };
     St sa, sb;
-    P2 raw[4];  // rows in flight: raw[p] holds row t = p+1 (mod 4)
+    P2 raw[PF];  // rows in flight: raw[p] holds row t = p+1 (mod PF)
     {
         P2 r0, r1;
         fetch(-1, ptr, r0);
@@ -96,8 +97,8 @@ __device__ __forceinline__ void lines2d_item(const typename Elem<DT>::T* __restr
         sa.eC = cmp2(C0, sa.pC);
     }
 #pragma unroll
-    for (int p = 0; p < 4; ++p) fetch(p + 1, ptr + (p + 2) * g.W, raw[p]);
-    ptr += 6 * g.W;  // row t = 5
+    for (int p = 0; p < PF; ++p) fetch(p + 1, ptr + (p + 2) * g.W, raw[p]);
+    ptr += (PF + 2) * g.W;  // row t = PF+1
 
     // row t arrives in V; every event of the row before it (state o) is booked
     auto step = [&](uint32_t V, const St& o, St& x) {
@@ -131,9 +132,9 @@ __device__ __forceinline__ void lines2d_item(const typename Elem<DT>::T* __restr
     int s = 0;
     // steady state: 4 steps per iteration, every refill (rows s+5 .. s+8)
     // inside the segment -- no guards
-    for (; s + 4 <= nm && s + 8 < tf; s += 4) {
+    for (; s + PF <= nm && s + 2 * PF < tf; s += PF) {
 #pragma unroll
-        for (int p = 0; p < 4; ++p) {
+        for (int p = 0; p < PF; ++p) {
             const uint32_t V = quant_in(raw[p]);
             raw[p] = load_pair<DT, VEC>(ptr + p * g.W, true, EDGE ? kk + 1 < Wi : true);
             if (p & 1)
@@ -141,21 +142,21 @@ __device__ __forceinline__ void lines2d_item(const typename Elem<DT>::T* __restr
             else
                 step(V, sa, sb);
         }
-        ptr += 4 * g.W;
+        ptr += PF * g.W;
     }
-    for (; s < nm; s += 4) {
+    for (; s < nm; s += PF) {
 #pragma unroll
-        for (int p = 0; p < 4; ++p) {
+        for (int p = 0; p < PF; ++p) {
             if (s + p < nm) {
                 const uint32_t V = quant_in(raw[p]);
-                fetch(s + p + 5, ptr + p * g.W, raw[p]);
+                fetch(s + p + PF + 1, ptr + p * g.W, raw[p]);
                 if (p & 1)
                     step(V, sb, sa);
                 else
                     step(V, sa, sb);
             }
         }
-        ptr += 4 * g.W;
+        ptr += PF * g.W;
     }
     if (nm < n) {  // at most one step: the absent row H
         if (nm & 1)
@@ -171,8 +172,11 @@ __device__ __forceinline__ void lines2d_item(const typename Elem<DT>::T* __restr
 // form one range cut evenly over the CTAs; inside a CTA each image's share is
 // cut evenly over the 16 warps, then the CTA folds that image's bins into
 // hist[image] (one __syncthreads pair per image).
-template <int DT, int QM, bool VEC>
-__global__ void __launch_bounds__(L2L_NTH, 2) lines2d_kernel(const typename Elem<DT>::T* __restrict__ buf, LGeo g,
+// PF / MINB: rows in flight per lane / CTAs per SM the registers are
+// budgeted for -- 8 / 1 for single images (latency-bound: more bytes in
+// flight per warp), 4 / 2 for batches (measured, profiles/r01/lines2d_notes.md).
+template <int DT, int QM, bool VEC, int PF, int MINB>
+__global__ void __launch_bounds__(L2L_NTH, MINB) lines2d_kernel(const typename Elem<DT>::T* __restrict__ buf, LGeo g,
                                                              QuantDev q, unsigned long long* __restrict__ hist)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -212,9 +216,9 @@ __global__ void __launch_bounds__(L2L_NTH, 2) lines2d_kernel(const typename Elem
             if (r0 >= r1) continue;
             const int k0 = t * 62 - 1;
             if (k0 >= 1 && k0 + 63 <= g.W)
-                lines2d_item<DT, QM, VEC, false>(img, g, q, tt, g.v0 + r0, g.v0 + r1, k0, lane);
+                lines2d_item<DT, QM, VEC, false, PF>(img, g, q, tt, g.v0 + r0, g.v0 + r1, k0, lane);
             else
-                lines2d_item<DT, QM, VEC, true>(img, g, q, tt, g.v0 + r0, g.v0 + r1, k0, lane);
+                lines2d_item<DT, QM, VEC, true, PF>(img, g, q, tt, g.v0 + r0, g.v0 + r1, k0, lane);
         }
         __syncthreads();
         // fold: C = sum of signature rows, E = sum (4 - u) rows, EC = plus -
@@ -271,7 +275,10 @@ static int launch_lines2d(const ft_window* win, int64_t H, int64_t W, int64_t v0
     QuantDev qd = qdev(qa);
     if (QM == FT_Q_POW2) qd.inv = M > 0 ? qd.scale / (float)M : 0.f;
     const size_t smem = (size_t)(LINES_PLUS + LINES_MINUS + g.hs);
-    auto kern = vec ? lines2d_kernel<DT, QM, true> : lines2d_kernel<DT, QM, false>;
+    using K = void (*)(const T*, LGeo, QuantDev, unsigned long long*);
+    const bool single = g.n_items == 1;
+    K kern = single ? (vec ? lines2d_kernel<DT, QM, true, 8, 1> : lines2d_kernel<DT, QM, false, 8, 1>)
+                    : (vec ? lines2d_kernel<DT, QM, true, 4, 2> : lines2d_kernel<DT, QM, false, 4, 2>);
     FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     FT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L2L_NTH, smem));

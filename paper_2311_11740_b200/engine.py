@@ -115,15 +115,15 @@ def new_lattice_hist(ndim, M, device, batch=1):
 
 
 def _use_lines2d(kernel, batch):
-    """ft_lines2d or ft_lattice2d for 2D rows 0..2.  Measured on B200
-    (profiles/r01/lines2d_notes.md): the line kernel wins on batches of
-    images (C3: 739 vs 682 Gpix/s), the lattice kernel on one large image
-    (C2: 548 vs 486).  ``kernel`` "lines" / "lattice" (or FT_2D_KERNEL)
-    forces one."""
+    """ft_lines2d or ft_lattice2d for 2D rows 0..2.  ft_lines2d is the default:
+    measured on B200 (ncu kernel durations, profiles/r01/lines2d_notes.md) it
+    beats the lattice kernel on one large image (C2: 85 vs 90 us) and on
+    batches (C3: 715 vs 779 us).  ``kernel`` "lines" / "lattice" (or
+    FT_2D_KERNEL) forces one."""
     force = kernel if kernel != "auto" else _os.environ.get("FT_2D_KERNEL", "auto")
     if force in ("lines", "lattice"):
         return force == "lines"
-    return batch > 1
+    return True
 
 
 def launch_lattice(ndim, x, shape, M, quant, rows=None, first=0, hist=None, batch=1, batch_stride=0,

@@ -10,16 +10,19 @@ ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 from paper_2311_11740_b200 import build as b  # noqa: E402
 
-objs = [p for p in sorted(b.BUILD.glob("*.o")) if p.stem != "ft_lines_f32p"]
+UNIT = "ft_lines_f32p"
+if len(sys.argv) > 1 and sys.argv[1].startswith("--unit="):
+    UNIT = sys.argv.pop(1).split("=", 1)[1]  # e.g. --unit=ft_lines2d
+objs = [p for p in sorted(b.BUILD.glob("*.o")) if p.stem != UNIT]
 
 
 def one(spec):
     name, flags = spec.split("=", 1)
     out = ROOT / "variants" / name
     out.mkdir(parents=True, exist_ok=True)
-    obj = out / "ft_lines_f32p.o"
+    obj = out / f"{UNIT}.o"
     cmd = [b.nvcc(), *b.ARCH, *b.NVCC_FLAGS, *flags.split(), "-Xptxas", "-v", "-c",
-           str(b.CSRC / "ft_lines_f32p.cu"), "-o", str(obj)]
+           str(b.CSRC / f"{UNIT}.cu"), "-o", str(obj)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode:
         return f"{name}: FAILED\n{r.stderr[-2000:]}"
