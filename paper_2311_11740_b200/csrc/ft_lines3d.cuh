@@ -15,8 +15,8 @@
 //   both, every family on the lattice positions (j, k) in [0, W] x [0, D].  A
 //   1D line of unit intervals has chi1 = sum over its cells of +1 (local min
 //   along i) / -1 (local max), so EC events are SPARSE: ~10% of cells per
-//   family on the benchmark fields, booked with predicated
-//   shared atomics whose inactive lanes touch no bank.
+//   family on the benchmark fields, booked with dummy-address
+//   shared atomics (lanes without an event all hit one merged word).
 // * Cubes and faces are booked once per cell by their per-cell signature, as
 //   in lattice3d_sig_kernel: the row u = #face neighbours activating before
 //   the cell (so F = sum (6 - u)), and -- when the 16-bit row offsets allow
@@ -34,7 +34,7 @@
 // pipe (95% busy there) stops being the limiter.  Same warp-strip register
 // march as lattice3d_rb_kernel (no staging, no CTA barrier).  Interior warp
 // strips run a guard-free loop (no load predicates, no sentinel selects, and
-// the FT_Q_POW2 quantizer is FMUL.SAT + FFMA.RM + F2I).
+// the FT_Q_POW2 quantizer is FMUL.SAT + FFMA2.RM + FADD2.RM, no F2I).
 //
 // Output rows (uint64 [3][M+2], accumulated): cells C, faces F, and
 // X = V - E = EC - F + C (two's complement; X may be negative).
@@ -434,15 +434,6 @@ static bool lines_ok(int M)
            lines_hs(M) + (M + 2) * 4 <= LINES_MINUS;
 }
 
-// Plane chunks: about 16 items per CTA (the warps of a CTA march
-// independently, so the kernel lasts as long as its busiest warp's strips),
-// marches of >= 64 planes.
-static int lines_chunk(int64_t rows, int64_t tiles, int64_t ctas)
-{
-    const int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>(cdiv(16 * ctas, std::max<int64_t>(tiles, 1)),
-                                                                   rows / 64));
-    return (int)cdiv(rows, nchunks);
-}
 
 #ifndef LINES_FUSED_DEF
 #define LINES_FUSED_DEF 1
@@ -473,11 +464,16 @@ static int launch_lines_kernel(const ft_window* win, LGeo g, const QuantDev& qd,
     for (int64_t j0 = 0; j0 <= g.W && g.rf_n < 4; j0 += LINES_R)
         if (j0 < 1 || j0 + LINES_R >= g.W) g.rf_j0[g.rf_n++] = (int)j0;
     const int64_t strips = (int64_t)g.tiles_k * g.rf_n;
-    // one warp per strip-chunk: chunks short enough to fill the grid's warps
-    g.e_chunk = lines_chunk(np, cdiv(strips, LINES_NTH / 32), cap);
+    // one warp per strip-chunk, the strip-planes spread over every warp of
+    // the grid (>= 8 planes per chunk): the CTA loops are evenly split, so an
+    // uneven share of boundary chunks would set the kernel's tail (C4a: one
+    // 65-plane chunk on 9 % of the warps cost ~20 %)
+    constexpr int NWC = LINES_NTH / 32;
+    const int64_t grid0 = std::max<int64_t>(1, std::min<int64_t>(cap, std::max<int64_t>(cdiv(work, 32), cdiv(strips, NWC))));
+    g.e_chunk = (int)std::min<int64_t>(np, std::max<int64_t>(8, cdiv(np * strips, grid0 * NWC)));
     g.e_items = MODE == 0 ? 0 : strips * cdiv(np, g.e_chunk);
     // the CTA ranges: >= 32 tile-planes per CTA
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(cap, std::max<int64_t>(cdiv(work, 32), cdiv(g.e_items, LINES_NTH / 32))));
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(cap, std::max<int64_t>(cdiv(work, 32), cdiv(g.e_items, NWC))));
     kern<<<(int)grid, LINES_NTH, smem, st>>>(static_cast<const T*>(win->data), g, qd,
                                             reinterpret_cast<unsigned long long*>(hist));
     FT_CUDA_TRY(cudaGetLastError());
