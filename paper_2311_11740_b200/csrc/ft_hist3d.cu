@@ -22,6 +22,8 @@
 // uniform 64-bit pointer bump.  Vertex columns j == W or k == D (the
 // high-side boundary) are done by a flat per-vertex kernel.
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "ft_common.cuh"
 #include "ft_tables.h"
@@ -215,6 +217,174 @@ __global__ void __launch_bounds__(NT3, 1) hist3d_tiled(const typename Elem<DT>::
     flush_hist(h, hist, 40 * M2);
 }
 
+// Same booking as hist3d_tiled with TWO k-adjacent vertices per thread: the
+// keys (level * 8 + slot <= 65535 for M + 1 <= 8190) of both vertices ride
+// in the 16-bit halves of one word, so the sort4 / merge44 networks run once
+// for the pair (VIMNMX.U16x2 min / max), the plane is read as aligned 32-bit
+// level pairs, and the per-plane barrier, loads and loop overhead serve twice
+// the vertices.  Tile 32 x 64 vertices (1024 threads).
+constexpr int TJP = 32, TKP = 64, NTP = TJP * TKP / 2;
+constexpr int PWP = TKP + 2;            // staged row pitch: cells k0-1 .. k0+64 (even)
+constexpr int PNP = (TJP + 1) * PWP;    // staged cells per plane
+constexpr int LDP = (PNP + NTP - 1) / NTP;
+
+__device__ __forceinline__ void cswap2(uint32_t& a, uint32_t& b)
+{
+    const uint32_t lo = __vminu2(a, b);
+    b = __vmaxu2(a, b);
+    a = lo;
+}
+__device__ __forceinline__ void sort4x2(uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d)
+{
+    cswap2(a, b);
+    cswap2(c, d);
+    cswap2(a, c);
+    cswap2(b, d);
+    cswap2(b, c);
+}
+__device__ __forceinline__ void merge44x2(uint32_t* k)
+{
+    cswap2(k[0], k[4]);
+    cswap2(k[1], k[5]);
+    cswap2(k[2], k[6]);
+    cswap2(k[3], k[7]);
+    cswap2(k[2], k[4]);
+    cswap2(k[3], k[5]);
+    cswap2(k[1], k[2]);
+    cswap2(k[3], k[4]);
+    cswap2(k[5], k[6]);
+}
+
+template <int DT, int QM>
+__global__ void __launch_bounds__(NTP, 1) hist3d_pair(const typename Elem<DT>::T* __restrict__ buf, Geo3 g,
+                                                      QuantDev q, const RankTables* __restrict__ rt,
+                                                      unsigned long long* __restrict__ hist)
+{
+    using T = typename Elem<DT>::T;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int M2 = g.M + 2;
+    uint32_t* h = reinterpret_cast<uint32_t*>(smem_raw);
+    uint32_t* ta = h + 40 * M2;
+    uint32_t* tb = ta + NTAB;
+    float* tt = reinterpret_cast<float*>(tb + NTAB);
+    uint16_t* pl = reinterpret_cast<uint16_t*>(tt + ((M2 + 1) & ~1));  // 4-byte aligned
+    init_shared3(h, ta, tb, tt, rt, q, M2, QM != FT_Q_IDENTITY);
+    __syncthreads();
+
+    const int tid = threadIdx.x;
+    const int ty = tid / (TKP / 2), tx = tid % (TKP / 2);
+    const int64_t per_chunk = (int64_t)g.tiles_j * g.tiles_k;
+    const int64_t it0 = g.n_items * blockIdx.x / gridDim.x;
+    const int64_t it1 = g.n_items * (blockIdx.x + 1) / gridDim.x;
+    const uint32_t sentinel = (uint32_t)g.M + 1;
+    const int64_t plane_elems = g.W * g.D;
+    const int Wi = (int)g.W, Di = (int)g.D;
+    const int w0i = (ty * PWP + 2 * tx) / 2, w1i = w0i + PWP / 2;  // 32-bit words of rows j-1, j
+
+    int lr[LDP], lc[LDP];
+#pragma unroll
+    for (int e = 0; e < LDP; ++e) {
+        const int idx = tid + e * NTP;
+        lr[e] = idx / PWP;
+        lc[e] = idx % PWP;
+    }
+
+    for (int64_t item = it0; item < it1; ++item) {
+        const int64_t ch = item / per_chunk;
+        const int rem = (int)(item - ch * per_chunk);
+        const int j0 = (rem / g.tiles_k) * TJP;
+        const int k0 = (rem % g.tiles_k) * TKP;
+        const int64_t ia = g.v0 + ch * g.chunk;
+        const int64_t ib = min(ia + (int64_t)g.chunk, g.v1);
+        const bool act_lo = (j0 + ty < Wi) && (k0 + 2 * tx < Di);
+        const bool act_hi = (j0 + ty < Wi) && (k0 + 2 * tx + 1 < Di);
+
+        int off[LDP];
+        bool ok[LDP];
+#pragma unroll
+        for (int e = 0; e < LDP; ++e) {
+            const int jj = j0 - 1 + lr[e], kk = k0 - 1 + lc[e];
+            ok[e] = (tid + e * NTP < PNP) && jj >= 0 && jj < Wi && kk >= 0 && kk < Di;
+            off[e] = ok[e] ? jj * Di + kk : 0;
+        }
+        T lv[PF3 + 1][LDP];
+        auto fetch = [&](int64_t p, T (&dst)[LDP]) {
+            const bool pin = p >= 0 && p < g.H;
+            const T* base = buf + (pin ? (p - g.first) * plane_elems : 0);
+#pragma unroll
+            for (int e = 0; e < LDP; ++e) {
+                dst[e] = T(0);
+                if (pin && ok[e]) dst[e] = ld_stream(base + off[e]);
+            }
+        };
+        auto store = [&](int64_t p, uint16_t* dstp, const T (&src)[LDP]) {
+            const bool pin = p >= 0 && p < g.H;
+#pragma unroll
+            for (int e = 0; e < LDP; ++e) {
+                const int idx = tid + e * NTP;
+                if (idx < PNP)
+                    dstp[idx] = (uint16_t)((pin && ok[e])
+                                               ? to_level<DT, QM>(src[e], tt, q.scale, q.bias, q.negate, g.M)
+                                               : sentinel);
+            }
+        };
+        // packed keys of one staged plane: slots (dj, dk) = (0,0) (1,0) (0,1)
+        // (1,1) -> 0, 2, 4, 6 (+ di); low half = vertex k, high half = k+1
+        auto keys = [&](const uint16_t* plane, uint32_t di, uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d) {
+            const uint32_t* p32 = reinterpret_cast<const uint32_t*>(plane);
+            const uint32_t r0 = p32[w0i], r0n = p32[w0i + 1], r1 = p32[w1i], r1n = p32[w1i + 1];
+            a = r0 * 8u + di * 0x10001u;
+            b = r1 * 8u + (2u + di) * 0x10001u;
+            c = __byte_perm(r0, r0n, 0x5432) * 8u + (4u + di) * 0x10001u;
+            d = __byte_perm(r1, r1n, 0x5432) * 8u + (6u + di) * 0x10001u;
+            sort4x2(a, b, c, d);
+        };
+        fetch(ia - 1, lv[0]);
+#pragma unroll
+        for (int s = 1; s <= PF3; ++s) fetch(ia - 1 + s, lv[s]);
+        store(ia - 1, pl, lv[0]);
+        __syncthreads();
+        uint32_t lo0, lo1, lo2, lo3;
+        keys(pl, 0u, lo0, lo1, lo2, lo3);
+
+        for (int64_t i = ia; i < ib; ++i) {
+            uint16_t* cur = pl + ((i - ia + 1) & 1) * PNP;
+            store(i, cur, lv[1]);
+#pragma unroll
+            for (int s = 1; s < PF3; ++s)
+#pragma unroll
+                for (int e = 0; e < LDP; ++e) lv[s][e] = lv[s + 1][e];
+            if (i + PF3 < ib) fetch(i + PF3, lv[PF3]);
+            __syncthreads();
+            uint32_t u0, u1, u2, u3;
+            keys(cur, 1u, u0, u1, u2, u3);
+            if (act_lo || act_hi) {
+                uint32_t k8[8] = {lo0, lo1, lo2, lo3, u0, u1, u2, u3};
+                merge44x2(k8);
+                if (act_lo) {
+                    uint32_t kl[8];
+#pragma unroll
+                    for (int s = 0; s < 8; ++s) kl[s] = k8[s] & 0xFFFFu;
+                    book3(h, ta, tb, kl, (uint32_t)M2);
+                }
+                if (act_hi) {
+                    uint32_t kh[8];
+#pragma unroll
+                    for (int s = 0; s < 8; ++s) kh[s] = k8[s] >> 16;
+                    book3(h, ta, tb, kh, (uint32_t)M2);
+                }
+            }
+            lo0 = u0 - 0x10001u;
+            lo1 = u1 - 0x10001u;
+            lo2 = u2 - 0x10001u;
+            lo3 = u3 - 0x10001u;
+        }
+        __syncthreads();
+    }
+    __syncthreads();
+    flush_hist(h, hist, 40 * M2);
+}
+
 // High-side boundary vertices (j == W, or k == D with j < W), flat.
 template <int DT, int QM>
 __global__ void __launch_bounds__(256) hist3d_edge(const typename Elem<DT>::T* __restrict__ buf, Geo3 g,
@@ -308,6 +478,7 @@ static const RankTables* device_rank_tables()
 }
 
 size_t hist3d_smem(int M) { return (size_t)(40 * (M + 2) + 2 * NTAB + (M + 2)) * 4 + 2 * PN3 * 2; }
+size_t hist3d_pair_smem(int M) { return (size_t)(40 * (M + 2) + 2 * NTAB + ((M + 3) & ~1)) * 4 + 2 * PNP * 2; }
 
 template <int DT, int QM>
 static int launch3(const ft_window* win, int64_t H, int64_t W, int64_t D, int64_t v0, int64_t v1,
@@ -327,7 +498,27 @@ static int launch3(const ft_window* win, int64_t H, int64_t W, int64_t D, int64_
     auto* out = reinterpret_cast<unsigned long long*>(hist);
     const int nsm = sm_count();
 
-    if (W > 0 && D > 0) {
+    static const char* which = getenv("FT_MAP3D");  // pair (default) | tiled (dev A/B)
+    if (W > 0 && D > 0 && !(which && !strcmp(which, "tiled")) && hist3d_pair_smem(M) <= 227 * 1024) {
+        auto kern = hist3d_pair<DT, QM>;
+        const size_t sm = hist3d_pair_smem(M);
+        FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        int per_sm = 0;
+        FT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NTP, sm));
+        if (per_sm < 1) return FT_ERR_ARG;
+        g.tiles_j = (int)cdiv(W, TJP);
+        g.tiles_k = (int)cdiv(D, TKP);
+        const int64_t tiles = (int64_t)g.tiles_j * g.tiles_k;
+        const int64_t rows = v1 - v0;
+        const int64_t grid_cap = (int64_t)nsm * per_sm;
+        int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>(cdiv(8 * grid_cap, tiles), rows / 32));
+        g.chunk = (int)cdiv(rows, nchunks);
+        nchunks = cdiv(rows, g.chunk);
+        g.n_items = tiles * nchunks;
+        const int grid = (int)std::min<int64_t>(grid_cap, g.n_items);
+        kern<<<grid, NTP, sm, st>>>(buf, g, q, rt, out);
+        FT_CUDA_TRY(cudaGetLastError());
+    } else if (W > 0 && D > 0) {
         auto kern = hist3d_tiled<DT, QM>;
         FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_tiled));
         int per_sm = 0;
