@@ -18,6 +18,7 @@
 #include <algorithm>
 
 #include "ft_common.cuh"
+#include "ft_lattice.cuh"
 #include "ft_tables.h"
 
 namespace ft {
@@ -181,6 +182,172 @@ __global__ void __launch_bounds__(256) hist2d_edge(const typename Elem<DT>::T* _
     }
 }
 
+// ------------------------------------------------ register-march map kernel
+// Same transition classes as hist2d_tiled (book2), but the register march of
+// the line kernels: a warp marches a strip of 62 vertex columns down the
+// rows, lane l holding the cells (kk, kk+1), kk = k0-1+2l, as packed 16-bit
+// level*4 words -- so the keys (level*4 + slot) of the lane's two vertices
+// ride in the halves of one word and sort4 / merge22 run once per pair
+// (VIMNMX.U16x2).  No staging, no barrier per row; every vertex column
+// 0..W is covered (no edge kernel).  Halves outside the vertex range or on a
+// halo lane book into a dummy row that is never flushed.
+constexpr int HM_NTH = 512;
+constexpr int HM_RB = 64;
+constexpr int HM_PF = 4;  // rows in flight per lane (even)
+
+__device__ __forceinline__ void hm_cswap2(uint32_t& a, uint32_t& b)
+{
+    const uint32_t lo = __vminu2(a, b);
+    b = __vmaxu2(a, b);
+    a = lo;
+}
+
+template <int DT, int QM, bool VEC, bool EDGE>
+__device__ __forceinline__ void hm_item(const typename Elem<DT>::T* __restrict__ img, const Geo2& g,
+                                        const QuantDev& q, const float* __restrict__ tt, uint32_t* __restrict__ h,
+                                        int64_t ia, int64_t ib, int k0, int lane)
+{
+    using P2 = typename Pair<DT>::T;
+    using T = typename Elem<DT>::T;
+    constexpr uint32_t FULL = 0xFFFFFFFFu, K1 = 0x10001u;
+    const int Wi = (int)g.W;
+    const uint32_t M2 = (uint32_t)g.M + 2u;
+    const uint32_t sent4 = ((uint32_t)g.M + 1u) * 4u;
+    const uint32_t S = sent4 * K1;
+    const int kk = k0 - 1 + 2 * lane;
+    // vertex columns kk (low half) and kk+1 (high half) that this lane books
+    const bool vlo = lane != 0 && kk >= 0 && kk <= Wi, vhi = lane != 31 && kk + 1 >= 0 && kk + 1 <= Wi;
+    const uint32_t vmask = __shfl_sync(FULL, (vlo ? 0x0000FFFFu : 0u) | (vhi ? 0xFFFF0000u : 0u), lane);
+    const uint32_t dummy = 6u * M2 * K1;
+    const bool okx = kk >= 0 && kk < Wi, oky = kk + 1 >= 0 && kk + 1 < Wi;
+    const int kc = !EDGE ? kk : VEC ? min(max(kk, 0), Wi - 2) : min(max(kk, 0), Wi - 1);
+    const int n = (int)(ib - ia);
+    // rows t = 0 .. n (row ia-1+t) exist iff t_lo <= t < t_hi; t < tf fetched
+    const int t_lo = (int)max((int64_t)0, 1 - ia);
+    const int t_hi = (int)min((int64_t)(n + 1), g.H - ia + 1);
+    const int tf = t_hi;
+    const T* ptr = img + ((ia - 1 - g.first) * g.W + kc);  // row ia-1 (t = 0)
+
+    auto fetch = [&](int t, const T* at, P2& dst) {
+        if (t >= t_lo && t < tf) dst = load_pair<DT, VEC>(at, true, EDGE ? kk + 1 < Wi : true);
+    };
+    auto quant_in = [&](const P2& src) -> uint32_t {
+        return pack_pair<DT, QM, 0>(src, !EDGE || okx, !EDGE || oky, tt, q, g.M, sent4);
+    };
+    // one vertex row: sorted NW / NE keys of the row above in a, c
+    uint32_t a, c;
+    auto step = [&](uint32_t V) {
+        const uint32_t Wm = shift_pair(__shfl_up_sync(FULL, V, 1), V);
+        uint32_t u0 = Wm + 2u * K1, u1 = V + 3u * K1;  // SW, SE
+        hm_cswap2(u0, u1);
+        uint32_t s0 = a, s1 = c, s2 = u0, s3 = u1;
+        hm_cswap2(s0, s2);
+        hm_cswap2(s1, s3);
+        hm_cswap2(s1, s2);
+        // class rows: s0 -> 0, s1 -> 1 (2 if diagonal), s2 -> 3 (4), s3 -> 5
+        const uint32_t diag = ((((s0 ^ s1) & 0x00030003u) + K1) >> 2) & K1;  // 1 per half iff slots {0,3} / {1,2}
+        const uint32_t i0 = (s0 >> 2) & 0x3FFF3FFFu;
+        const uint32_t i1 = ((s1 >> 2) & 0x3FFF3FFFu) + (K1 + diag) * M2;
+        const uint32_t i2 = ((s2 >> 2) & 0x3FFF3FFFu) + (3u * K1 + diag) * M2;
+        const uint32_t i3 = ((s3 >> 2) & 0x3FFF3FFFu) + 5u * M2 * K1;
+        const uint32_t w[4] = {i0, i1, i2, i3};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const uint32_t x = (w[e] & vmask) | (dummy & ~vmask);
+            atomicAdd(&h[x & 0xFFFFu], 1u);
+            atomicAdd(&h[x >> 16], 1u);
+        }
+        a = u0 - 2u * K1;
+        c = u1 - 2u * K1;
+    };
+
+    P2 raw[HM_PF];
+    {
+        P2 r0;
+        fetch(0, ptr, r0);
+        const uint32_t V0 = t_lo <= 0 && 0 < t_hi ? quant_in(r0) : S;  // row ia-1
+        const uint32_t Wm0 = shift_pair(__shfl_up_sync(FULL, V0, 1), V0);
+        a = Wm0;            // NW (slot 0)
+        c = V0 + K1;        // NE (slot 1)
+        hm_cswap2(a, c);
+    }
+#pragma unroll
+    for (int p = 0; p < HM_PF; ++p) fetch(p + 1, ptr + (p + 1) * g.W, raw[p]);
+    ptr += (HM_PF + 1) * g.W;  // row t = PF+1
+    const int nm = min(n, t_hi - 1);  // steps s < nm see an existing row t = s+1
+    int s = 0;
+    for (; s + HM_PF <= nm && s + 2 * HM_PF < tf; s += HM_PF) {
+#pragma unroll
+        for (int p = 0; p < HM_PF; ++p) {
+            const uint32_t V = quant_in(raw[p]);
+            raw[p] = load_pair<DT, VEC>(ptr + p * g.W, true, EDGE ? kk + 1 < Wi : true);
+            step(V);
+        }
+        ptr += HM_PF * g.W;
+    }
+    for (; s < nm; s += HM_PF) {
+#pragma unroll
+        for (int p = 0; p < HM_PF; ++p) {
+            if (s + p < nm) {
+                const uint32_t V = quant_in(raw[p]);
+                fetch(s + p + HM_PF + 1, ptr + p * g.W, raw[p]);
+                step(V);
+            }
+        }
+        ptr += HM_PF * g.W;
+    }
+    if (nm < n) step(S);  // vertex row H: the absent row below
+}
+
+template <int DT, int QM, bool VEC>
+__global__ void __launch_bounds__(HM_NTH, 2) hist2d_march(const typename Elem<DT>::T* __restrict__ buf, Geo2 g,
+                                                         QuantDev q, unsigned long long* __restrict__ hist)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int M2 = g.M + 2;
+    uint32_t* h = reinterpret_cast<uint32_t*>(smem_raw);  // 6 class rows + the dummy row
+    float* tt = reinterpret_cast<float*>(h + 7 * M2);
+    for (int i = threadIdx.x; i < 7 * M2; i += blockDim.x) h[i] = 0;
+    if (QM != FT_Q_IDENTITY)
+        for (int i = threadIdx.x; i < M2; i += blockDim.x) tt[i] = q.tt[i];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NW = HM_NTH / 32;
+    const int64_t nrows = g.v1 - g.v0;
+    const int ntiles = g.tiles;
+    const int64_t Timg = cdiv(nrows, (int64_t)HM_RB) * ntiles * HM_RB;
+    const int64_t total = g.batch * Timg;
+    const int64_t U0 = total * blockIdx.x / gridDim.x, U1 = total * (blockIdx.x + 1) / gridDim.x;
+    for (int64_t b = U0 / Timg; b < g.batch && b * Timg < U1; ++b) {
+        const int64_t a = max(U0, b * Timg) - b * Timg, e = min(U1, (b + 1) * Timg) - b * Timg;
+        const int64_t wa = a + (e - a) * warp / NW, we = a + (e - a) * (warp + 1) / NW;
+        const typename Elem<DT>::T* img = buf + b * g.bstride;
+        for (int64_t u = wa; u < we;) {
+            const int64_t piece = u / HM_RB;
+            const int r = (int)(u - piece * HM_RB);
+            const int64_t len = min(we - u, (int64_t)(HM_RB - r));
+            u += len;
+            const int64_t rb = piece / ntiles;
+            const int t = (int)(piece - rb * ntiles);
+            const int64_t r0 = rb * HM_RB + r, r1 = min(r0 + len, nrows);
+            if (r0 >= r1) continue;
+            const int k0 = t * 62 - 1;
+            if (k0 >= 1 && k0 + 63 <= g.W)
+                hm_item<DT, QM, VEC, false>(img, g, q, tt, h, g.v0 + r0, g.v0 + r1, k0, lane);
+            else
+                hm_item<DT, QM, VEC, true>(img, g, q, tt, h, g.v0 + r0, g.v0 + r1, k0, lane);
+        }
+        __syncthreads();
+        unsigned long long* out = hist + b * FT_NCLASS_2D * M2;
+        for (int i = threadIdx.x; i < 7 * M2; i += blockDim.x) {
+            const uint32_t v = h[i];
+            h[i] = 0;
+            if (v && i < 6 * M2) atomicAdd(&out[i], (unsigned long long)v);
+        }
+        __syncthreads();
+    }
+}
+
 static int sm_count2()
 {
     int dev = 0, n = kSMs;
@@ -204,6 +371,25 @@ static int launch2(const ft_window* win, int64_t H, int64_t W, int64_t v0, int64
     const size_t smem = (size_t)(FT_NCLASS_2D * M2 + M2) * 4 + 2 * RW2 * sizeof(uint16_t);
     auto* out = reinterpret_cast<unsigned long long*>(hist);
     const int nsm = sm_count2();
+    static const char* which = getenv("FT_MAP2D");  // march (default) | tiled (dev A/B)
+    if (!(which && !strcmp(which, "tiled")) && 7 * M2 <= 0xFFFF && (size_t)8 * M2 * 4 <= 227 * 1024) {
+        // register march: every vertex column 0..W, no edge kernel
+        const bool vec = W % 2 == 0 && (g.batch <= 1 || g.bstride % 2 == 0) &&
+                         reinterpret_cast<uintptr_t>(buf) % (2 * sizeof(T)) == 0;
+        auto kern = vec ? hist2d_march<DT, QM, true> : hist2d_march<DT, QM, false>;
+        const size_t sm = (size_t)8 * M2 * 4;
+        FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        int per_sm = 0;
+        FT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, HM_NTH, sm));
+        if (per_sm < 1) return FT_ERR_ARG;
+        g.tiles = (int)((W + 1) / 62 + 1);  // tile t: vertex columns 62 t - 1 .. 62 t + 60
+        const int64_t units = g.batch * cdiv(v1 - v0, (int64_t)HM_RB) * g.tiles * HM_RB;
+        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * per_sm,
+                                                                    cdiv(units, (int64_t)(HM_NTH / 32) * HM_RB)));
+        kern<<<(int)grid, HM_NTH, sm, st>>>(buf, g, q, out);
+        FT_CUDA_TRY(cudaGetLastError());
+        return FT_OK;
+    }
     {
         auto kern = hist2d_tiled<DT, QM>;
         FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
