@@ -26,6 +26,7 @@
 #include <cstring>
 
 #include "ft_common.cuh"
+#include "ft_lattice.cuh"
 #include "ft_tables.h"
 
 namespace ft {
@@ -385,6 +386,167 @@ __global__ void __launch_bounds__(NTP, 1) hist3d_pair(const typename Elem<DT>::T
     flush_hist(h, hist, 40 * M2);
 }
 
+// ------------------------------------------------ register-march map kernel
+// The booking of hist3d_tiled / hist3d_pair on the register march of the line
+// kernels: a warp marches a strip of HMR vertex rows x 62 vertex columns
+// along i; lane l holds the cells (kk, kk+1), kk = k0-1+2l, of HMR+1 cell rows
+// as packed level*8 words, so the keys (level*8 + slot) of its two vertices
+// share one word and sort4 / merge44 run once per pair (VIMNMX.U16x2); the
+// -k cells are one shuffle away.  No staging, no barrier per plane; every
+// vertex (j, k) in [0, W] x [0, D] is covered (no edge kernel).
+constexpr int HMR = 4;          // vertex rows per warp strip
+constexpr int HM3_NTH = 512;    // 16 warps: 64 vertex rows per CTA tile
+
+template <int DT, int QM, bool VEC, bool EDGE>
+__device__ __forceinline__ void hm3_item(const typename Elem<DT>::T* __restrict__ buf, const Geo3& g,
+                                         const QuantDev& q, const float* __restrict__ tt,
+                                         uint32_t* __restrict__ h, const uint32_t* __restrict__ ta,
+                                         const uint32_t* __restrict__ tb, int64_t ia, int64_t ib, int j0, int k0,
+                                         int lane)
+{
+    using P2 = typename Pair<DT>::T;
+    using T = typename Elem<DT>::T;
+    constexpr int NR = HMR + 1;  // cell rows j0-1 .. j0+HMR-1
+    constexpr uint32_t FULL = 0xFFFFFFFFu, K1 = 0x10001u;
+    const int Wi = (int)g.W, Di = (int)g.D;
+    const uint32_t M2 = (uint32_t)g.M + 2u;
+    const uint32_t sent8 = ((uint32_t)g.M + 1u) * 8u;
+    const uint32_t S = sent8 * K1;
+    const int kk = k0 - 1 + 2 * lane;
+    const bool clo = lane != 0 && kk >= 0 && kk <= Di, chi = lane != 31 && kk + 1 >= 0 && kk + 1 <= Di;
+    const bool okx = kk >= 0 && kk < Di, oky = kk + 1 >= 0 && kk + 1 < Di;
+    const int kc = !EDGE ? kk : VEC ? min(max(kk, 0), Di - 2) : min(max(kk, 0), Di - 1);
+    uint32_t rowok = (1u << NR) - 1u;
+    if constexpr (EDGE) {
+        rowok = 0;
+#pragma unroll
+        for (int c = 0; c < NR; ++c) rowok |= (j0 - 1 + c >= 0 && j0 - 1 + c < Wi) ? 1u << c : 0u;
+    }
+    bool vrow[HMR];
+#pragma unroll
+    for (int v = 0; v < HMR; ++v) vrow[v] = j0 + v <= Wi;
+    const int64_t pe = g.W * g.D;
+    const int n = (int)(ib - ia);
+    // planes t = 0 .. n (plane ia-1+t) exist iff t_lo <= t < t_hi
+    const int t_lo = (int)max((int64_t)0, 1 - ia);
+    const int t_hi = (int)min((int64_t)(n + 1), g.H - ia + 1);
+    const T* ptr = buf + ((ia - 1 - g.first) * pe + (int64_t)(j0 - 1) * Di + kc);
+
+    auto fetch = [&](int t, const T* at, P2(&dst)[NR]) {
+        if (t >= t_lo && t < t_hi) {
+#pragma unroll
+            for (int c = 0; c < NR; ++c)
+                if (!EDGE || ((rowok >> c) & 1u)) dst[c] = load_pair<DT, VEC>(at + c * Di, true, EDGE ? kk + 1 < Di : true);
+        }
+    };
+    // packed keys (level*8) of one plane's cell rows: V (cells kk, kk+1) and
+    // Wm (cells kk-1, kk)
+    auto planes = [&](int t, const P2(&src)[NR], uint32_t(&V)[NR], uint32_t(&Wm)[NR]) {
+        const bool exists = t >= t_lo && t < t_hi;
+#pragma unroll
+        for (int c = 0; c < NR; ++c) {
+            uint32_t v = pack_pair<DT, QM, 1>(src[c], !EDGE || okx, !EDGE || oky, tt, q, g.M, sent8);
+            if (EDGE && !((rowok >> c) & 1u)) v = S;
+            V[c] = exists ? v : S;
+            Wm[c] = shift_pair(__shfl_up_sync(FULL, V[c], 1), V[c]);
+        }
+    };
+    // sorted keys of vertex row v from a plane: slots di + 2 dj + 4 dk
+    auto keys4 = [&](const uint32_t(&V)[NR], const uint32_t(&Wm)[NR], int v, uint32_t di, uint32_t(&k)[4]) {
+        k[0] = Wm[v] + di * K1;
+        k[1] = Wm[v + 1] + (2u + di) * K1;
+        k[2] = V[v] + (4u + di) * K1;
+        k[3] = V[v + 1] + (6u + di) * K1;
+        sort4x2(k[0], k[1], k[2], k[3]);
+    };
+
+    uint32_t prev[HMR][4];
+    P2 ra[NR], rb[NR];
+    {
+        uint32_t V[NR], Wm[NR];
+        fetch(0, ptr, ra);
+        planes(0, ra, V, Wm);
+#pragma unroll
+        for (int v = 0; v < HMR; ++v) keys4(V, Wm, v, 0u, prev[v]);
+    }
+    fetch(1, ptr + pe, ra);
+    fetch(2, ptr + 2 * pe, rb);
+    ptr += 3 * pe;  // next fetch: t = 3
+    auto step = [&](int t, const P2(&src)[NR]) {
+        uint32_t V[NR], Wm[NR];
+        planes(t, src, V, Wm);
+#pragma unroll
+        for (int v = 0; v < HMR; ++v) {
+            uint32_t u[4];
+            keys4(V, Wm, v, 1u, u);
+            uint32_t k8[8] = {prev[v][0], prev[v][1], prev[v][2], prev[v][3], u[0], u[1], u[2], u[3]};
+            merge44x2(k8);
+            if (vrow[v] && clo) {
+                uint32_t kl[8];
+#pragma unroll
+                for (int s = 0; s < 8; ++s) kl[s] = k8[s] & 0xFFFFu;
+                book3(h, ta, tb, kl, M2);
+            }
+            if (vrow[v] && chi) {
+                uint32_t kh[8];
+#pragma unroll
+                for (int s = 0; s < 8; ++s) kh[s] = k8[s] >> 16;
+                book3(h, ta, tb, kh, M2);
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) prev[v][e] = u[e] - K1;
+        }
+    };
+    // vertex planes ia + s, s = 0 .. n-1, each reading cell plane t = s+1
+    int s = 0;
+    for (; s < n; s += 2) {
+        step(s + 1, ra);
+        if (s + 3 <= n) fetch(s + 3, ptr, ra);
+        ptr += pe;
+        if (s + 1 >= n) break;
+        step(s + 2, rb);
+        if (s + 4 <= n) fetch(s + 4, ptr, rb);
+        ptr += pe;
+    }
+}
+
+template <int DT, int QM, bool VEC>
+__global__ void __launch_bounds__(HM3_NTH, 1) hist3d_march(const typename Elem<DT>::T* __restrict__ buf, Geo3 g,
+                                                          QuantDev q, const RankTables* __restrict__ rt,
+                                                          unsigned long long* __restrict__ hist)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int M2 = g.M + 2;
+    uint32_t* h = reinterpret_cast<uint32_t*>(smem_raw);
+    uint32_t* ta = h + 40 * M2;
+    uint32_t* tb = ta + NTAB;
+    float* tt = reinterpret_cast<float*>(tb + NTAB);
+    init_shared3(h, ta, tb, tt, rt, q, M2, QM != FT_Q_IDENTITY);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int TJ = (HM3_NTH / 32) * HMR;
+    const int64_t np = g.v1 - g.v0;
+    const int64_t T = (int64_t)g.tiles_j * g.tiles_k * np;  // (tile, plane) units, tile-major
+    const int64_t u_end = T * (blockIdx.x + 1) / gridDim.x;
+    for (int64_t u = T * blockIdx.x / gridDim.x; u < u_end;) {
+        const int tile = (int)(u / np);
+        const int64_t p = u - (int64_t)tile * np;
+        const int64_t len = min(u_end - u, np - p);
+        u += len;
+        const int tj = tile / g.tiles_k;
+        const int j0 = tj * TJ + warp * HMR;
+        const int k0 = (tile - tj * g.tiles_k) * 62 - 1;
+        if (j0 > g.W) continue;
+        const int64_t ia = g.v0 + p;
+        if (j0 >= 1 && j0 + HMR <= g.W && k0 >= 1 && k0 + 63 <= g.D)
+            hm3_item<DT, QM, VEC, false>(buf, g, q, tt, h, ta, tb, ia, ia + len, j0, k0, lane);
+        else
+            hm3_item<DT, QM, VEC, true>(buf, g, q, tt, h, ta, tb, ia, ia + len, j0, k0, lane);
+    }
+    __syncthreads();
+    flush_hist(h, hist, 40 * M2);
+}
+
 // High-side boundary vertices (j == W, or k == D with j < W), flat.
 template <int DT, int QM>
 __global__ void __launch_bounds__(256) hist3d_edge(const typename Elem<DT>::T* __restrict__ buf, Geo3 g,
@@ -498,7 +660,24 @@ static int launch3(const ft_window* win, int64_t H, int64_t W, int64_t D, int64_
     auto* out = reinterpret_cast<unsigned long long*>(hist);
     const int nsm = sm_count();
 
-    static const char* which = getenv("FT_MAP3D");  // pair (default) | tiled (dev A/B)
+    static const char* which = getenv("FT_MAP3D");  // march (default) | pair | tiled (dev A/B)
+    const size_t sm_march = (size_t)(40 * M2 + 2 * NTAB + M2) * 4;
+    if ((!which || !strcmp(which, "march")) && sm_march <= 227 * 1024) {
+        // register march: every vertex (j, k) in [0, W] x [0, D], no edge kernel
+        const bool vec = D % 2 == 0 && reinterpret_cast<uintptr_t>(buf) % (2 * sizeof(T)) == 0;
+        auto kern = vec ? hist3d_march<DT, QM, true> : hist3d_march<DT, QM, false>;
+        FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_march));
+        int per_sm = 0;
+        FT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, HM3_NTH, sm_march));
+        if (per_sm < 1) return FT_ERR_ARG;
+        g.tiles_j = (int)cdiv(W + 1, (HM3_NTH / 32) * HMR);
+        g.tiles_k = (int)((D + 1) / 62 + 1);  // tile t: vertex columns 62 t - 1 .. 62 t + 60
+        const int64_t work = (int64_t)g.tiles_j * g.tiles_k * (v1 - v0);
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * per_sm, cdiv(work, 32)));
+        kern<<<grid, HM3_NTH, sm_march, st>>>(buf, g, q, rt, out);
+        FT_CUDA_TRY(cudaGetLastError());
+        return FT_OK;
+    }
     if (W > 0 && D > 0 && !(which && !strcmp(which, "tiled")) && hist3d_pair_smem(M) <= 227 * 1024) {
         auto kern = hist3d_pair<DT, QM>;
         const size_t sm = hist3d_pair_smem(M);
