@@ -397,6 +397,39 @@ __global__ void __launch_bounds__(NTP, 1) hist3d_pair(const typename Elem<DT>::T
 constexpr int HMR = 4;          // vertex rows per warp strip
 constexpr int HM3_NTH = 512;    // 16 warps: 64 vertex rows per CTA tile
 
+// book3 for a packed vertex pair: the rank-group slot indices of both halves
+// in one pass (12 bits each), levels extracted per half.
+__device__ __forceinline__ void book3_pair(uint32_t* __restrict__ h, const uint32_t* __restrict__ ta,
+                                           const uint32_t* __restrict__ tb, const uint32_t (&k)[8], uint32_t M2,
+                                           bool lo, bool hi)
+{
+    constexpr uint32_t S7 = 0x00070007u;
+    const uint32_t ia = ((k[0] & S7) << 9) | ((k[1] & S7) << 6) | ((k[2] & S7) << 3) | (k[3] & S7);
+    const uint32_t ib = ((k[4] & S7) << 9) | ((k[5] & S7) << 6) | ((k[6] & S7) << 3) | (k[7] & S7);
+    if (lo) {
+        const uint32_t ea = ta[ia & 0xFFFu], eb = tb[ib & 0xFFFu];
+        atomicAdd(&h[(k[0] & 0xFFFFu) >> 3], 1u);
+        atomicAdd(&h[(ea & 0xFFu) * M2 + ((k[1] & 0xFFFFu) >> 3)], 1u);
+        atomicAdd(&h[((ea >> 8) & 0xFFu) * M2 + ((k[2] & 0xFFFFu) >> 3)], 1u);
+        atomicAdd(&h[(ea >> 16) * M2 + ((k[3] & 0xFFFFu) >> 3)], 1u);
+        atomicAdd(&h[(eb & 0xFFu) * M2 + ((k[4] & 0xFFFFu) >> 3)], 1u);
+        atomicAdd(&h[((eb >> 8) & 0xFFu) * M2 + ((k[5] & 0xFFFFu) >> 3)], 1u);
+        atomicAdd(&h[(eb >> 16) * M2 + ((k[6] & 0xFFFFu) >> 3)], 1u);
+        atomicAdd(&h[39u * M2 + ((k[7] & 0xFFFFu) >> 3)], 1u);
+    }
+    if (hi) {
+        const uint32_t ea = ta[ia >> 16], eb = tb[ib >> 16];
+        atomicAdd(&h[k[0] >> 19], 1u);
+        atomicAdd(&h[(ea & 0xFFu) * M2 + (k[1] >> 19)], 1u);
+        atomicAdd(&h[((ea >> 8) & 0xFFu) * M2 + (k[2] >> 19)], 1u);
+        atomicAdd(&h[(ea >> 16) * M2 + (k[3] >> 19)], 1u);
+        atomicAdd(&h[(eb & 0xFFu) * M2 + (k[4] >> 19)], 1u);
+        atomicAdd(&h[((eb >> 8) & 0xFFu) * M2 + (k[5] >> 19)], 1u);
+        atomicAdd(&h[(eb >> 16) * M2 + (k[6] >> 19)], 1u);
+        atomicAdd(&h[39u * M2 + (k[7] >> 19)], 1u);
+    }
+}
+
 template <int DT, int QM, bool VEC, bool EDGE>
 __device__ __forceinline__ void hm3_item(const typename Elem<DT>::T* __restrict__ buf, const Geo3& g,
                                          const QuantDev& q, const float* __restrict__ tt,
@@ -481,18 +514,7 @@ __device__ __forceinline__ void hm3_item(const typename Elem<DT>::T* __restrict_
             keys4(V, Wm, v, 1u, u);
             uint32_t k8[8] = {prev[v][0], prev[v][1], prev[v][2], prev[v][3], u[0], u[1], u[2], u[3]};
             merge44x2(k8);
-            if (vrow[v] && clo) {
-                uint32_t kl[8];
-#pragma unroll
-                for (int s = 0; s < 8; ++s) kl[s] = k8[s] & 0xFFFFu;
-                book3(h, ta, tb, kl, M2);
-            }
-            if (vrow[v] && chi) {
-                uint32_t kh[8];
-#pragma unroll
-                for (int s = 0; s < 8; ++s) kh[s] = k8[s] >> 16;
-                book3(h, ta, tb, kh, M2);
-            }
+            book3_pair(h, ta, tb, k8, M2, vrow[v] && clo, vrow[v] && chi);
 #pragma unroll
             for (int e = 0; e < 4; ++e) prev[v][e] = u[e] - K1;
         }
