@@ -112,6 +112,16 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def cpu_model():
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -127,13 +137,17 @@ def cpu_reference(x_host, M, lo_hi, descs, budget_s=15.0, threads=None):
     H, W, D = x_host.shape
     tables = [oracle.BUILTIN_3D[(d, "26C" if d == "ec" else None)] for d in descs]
 
+    last = [None]
+
     def run(nplanes):
         sample = np.ascontiguousarray(x_host[:nplanes])
         t0 = time.perf_counter()
         q_in, q_out = oracle.gather3d(sample, M, value_range=lo_hi, workers=threads, rows=(0, nplanes))
         for w in tables:
             oracle.descriptor_numerators(q_in, q_out, M, w)
-        return time.perf_counter() - t0
+        dt = time.perf_counter() - t0
+        last[0] = (q_in, q_out)
+        return dt
 
     # the oracle splits vertex rows over threads like the reference
     # (_parallel.py:8-24): keep >= 4 planes per thread so all cores work
@@ -143,9 +157,9 @@ def cpu_reference(x_host, M, lo_hi, descs, budget_s=15.0, threads=None):
         n = min(H, n * 2)
         t = run(n)
     n_final = max(min(H, 4 * threads), min(H, int(n * budget_s / max(t, 1e-6))))
-    t = run(n_final)
+    t, maps = run(n_final), last[0]
     cells = n_final * W * D
-    return cells / t / 1e9, cells, t, threads
+    return cells / t / 1e9, cells, t, threads, n_final, maps
 
 
 def main():
@@ -339,10 +353,19 @@ def main():
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         xs = host.numpy() if e2e is not None else x.cpu().numpy()
-        v, n, secs, thr = cpu_reference(xs, M, (0.0, 1.0), descs, args.cpu_budget)
-        cpu = {"value": round(v, 6), "unit": "Gvoxels/s", "cores": thr, "kind": "port",
+        v, n, secs, thr, nplanes, (oq_in, oq_out) = cpu_reference(xs, M, (0.0, 1.0), descs, args.cpu_budget)
+        cpu = {"value": round(v, 6), "unit": "Gvoxels/s", "cores": thr, "kind": "port", "cpu_model": cpu_model(),
                "sample": f"{n // (W * D)} planes x {W}x{D} of the same field ({n} voxels, {secs:.1f} s), "
                          "oracle/ft_oracle.c gather + curves"}
+        # parity on the sample: the drop-in map kernel on the same planes and
+        # vertex rows [0, nplanes) must equal the oracle's maps bit for bit
+        xd = engine.to_device(xs[:nplanes], dev)
+        sh = engine.launch_hist(3, xd, (nplanes, W, D), M, quant, rows=(0, nplanes))
+        sq_in, sq_out, _ = engine.finalize(3, M, sh, maps=True)
+        checks["oracle_sample_maps_equal"] = bool(np.array_equal(engine.as_uint64(sq_in), oq_in)
+                                                  and np.array_equal(engine.as_uint64(sq_out), oq_out))
+        checks["oracle_sample"] = f"vertex rows [0, {nplanes}) of the benchmark field"
+        del xd, sh
 
     if rank == 0:
         peak, peak_kind = peaks()
@@ -364,7 +387,7 @@ def main():
                             "kernel_ms": round(kms, 4), "peak_source": peak_kind,
                             "algorithmic_bytes_per_launch": int(bytes_per_launch)},
                "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": 2 * args.steps,
-               "map_path": {"kernel": "hist3d_tiled + hist3d_edge (transition-class maps, gather_3d_*)",
+               "map_path": {"kernel": "hist3d_march (transition-class maps, gather_3d_*)",
                             "value": round(map_gvox, 4), "unit": "Gvoxels/s",
                             "kernel_ms": round(statistics.median(map_ms), 4)},
                "clocks": clk.summary()}
@@ -411,7 +434,7 @@ def run_reference(args, shape, sigma, M, descs, config, ws):
         x = np.random.default_rng(args.seed).random((nplanes, W, D), dtype=np.float32)
     times = []
     for it in range(args.warmup + args.steps):
-        v, n, secs, thr = cpu_reference(x, M, (0.0, 1.0), descs, budget_s=max(2.0, args.cpu_budget / 3))
+        v, n, secs, thr, _, _ = cpu_reference(x, M, (0.0, 1.0), descs, budget_s=max(2.0, args.cpu_budget / 3))
         if it >= args.warmup:
             times.append(v)
     v = statistics.mean(times)
@@ -420,7 +443,7 @@ def run_reference(args, shape, sigma, M, descs, config, ws):
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32 in, int64 levels",
            "data": "synthetic (same seeded GRF slab)", "config": config,
            "cpu_baseline": {"value": round(v, 6), "unit": "Gvoxels/s", "cores": thr, "kind": "port",
-                            "sample": f"{n // (W * D)} planes x {W}x{D} per step (bounded sample)"},
+                            "cpu_model": cpu_model(), "sample": f"{n // (W * D)} planes x {W}x{D} per step (bounded sample)"},
            "e2e": {"value": round(v, 6), "unit": "Gvoxels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
 

@@ -61,6 +61,23 @@ def _stream_ptr(device):
     return ctypes.c_void_p(torch().cuda.current_stream(device).cuda_stream)
 
 
+def on_device(device):
+    """Make ``device`` the thread's current CUDA device for a library call.
+
+    The C library takes the device from the calling thread (rank tables, SM
+    count, kernel attributes, the launch itself) and the stream handle of
+    torch's default stream is NULL, so every call that touches a tensor on
+    cuda:N must run with cuda:N current (cuda:1 tensors launched
+    from a cuda:0 thread would fault or race)."""
+    return torch().cuda.device(device)
+
+
+def _rows_held(ndim, x, batch):
+    """Rows (2D) / planes (3D) the window tensor holds: an (N, H, W) image
+    stack holds H rows for any N, including N == 1."""
+    return x.shape[-2] if ndim == 2 and x.dim() == 3 else x.shape[0]
+
+
 def to_device(array, device, pinned=True):
     """numpy/torch array -> contiguous CUDA tensor (pinned-staged H2D)."""
     t = torch()
@@ -93,13 +110,20 @@ def launch_hist(ndim, x, shape, M, quant, rows=None, first=0, hist=None, batch=1
     v0, v1 = rows if rows is not None else (0, H + 1)
     if hist is None:
         hist = new_hist(ndim, M, dev, batch)
-    count = x.shape[1] if batch > 1 else x.shape[0]
+    count = _rows_held(ndim, x, batch)
     win = _lib.ft_window(ctypes.c_void_p(x.data_ptr()), dtype_code(x), int(first), int(count),
                          int(batch), int(batch_stride))
-    qs, keep = device_struct(quant, dev)
-    st = _stream_ptr(dev)
+    with on_device(dev):
+        qs, keep = device_struct(quant, dev)
+        rc = _hist_call(L, ndim, win, H, shape, v0, v1, qs, M, hist, _stream_ptr(dev))
+    del keep
+    _lib.check(rc, f"ft_hist{ndim}d")
+    return hist
+
+
+def _hist_call(L, ndim, win, H, shape, v0, v1, qs, M, hist, st):
     if ndim == 2:
-        rc = L.ft_hist2d(ctypes.byref(win), H, shape[1], v0, v1, ctypes.byref(qs), M,
+        return L.ft_hist2d(ctypes.byref(win), H, shape[1], v0, v1, ctypes.byref(qs), M,
                          ctypes.c_void_p(hist.data_ptr()), st)
     else:
         rc = L.ft_hist3d(ctypes.byref(win), H, shape[1], shape[2], v0, v1, ctypes.byref(qs), M,
@@ -137,26 +161,27 @@ def launch_lattice(ndim, x, shape, M, quant, rows=None, first=0, hist=None, batc
     v0, v1 = rows if rows is not None else (0, H + 1)
     if hist is None:
         hist = new_lattice_hist(ndim, M, dev, batch)
-    count = x.shape[1] if batch > 1 else x.shape[0]
+    count = _rows_held(ndim, x, batch)
     win = _lib.ft_window(ctypes.c_void_p(x.data_ptr()), dtype_code(x), int(first), int(count),
                          int(batch), int(batch_stride))
-    qs, keep = device_struct(quant, dev)
-    st = _stream_ptr(dev)
-    if ndim == 2 and not maxes and lines2d_ok(M) and _use_lines2d(kernel, batch):
-        # rows 0..2 by line decomposition (ft_lines2d): fewer shared atomics
-        rc = L.ft_lines2d(ctypes.byref(win), H, shape[1], v0, v1, ctypes.byref(qs), M,
-                          ctypes.c_void_p(hist.data_ptr()), st)
-        del keep
-        _lib.check(rc, "ft_lines2d")
-        return hist
-    if ndim == 2:
-        rc = L.ft_lattice2d(ctypes.byref(win), H, shape[1], v0, v1, ctypes.byref(qs), M, int(maxes),
-                            ctypes.c_void_p(hist.data_ptr()), st)
-    else:
-        rc = L.ft_lattice3d(ctypes.byref(win), H, shape[1], shape[2], v0, v1, ctypes.byref(qs), M,
-                            ctypes.c_void_p(hist.data_ptr()), st)
+    with on_device(dev):
+        qs, keep = device_struct(quant, dev)
+        st = _stream_ptr(dev)
+        if ndim == 2 and not maxes and lines2d_ok(M) and _use_lines2d(kernel, batch):
+            # rows 0..2 by line decomposition (ft_lines2d): fewer shared atomics
+            name = "ft_lines2d"
+            rc = L.ft_lines2d(ctypes.byref(win), H, shape[1], v0, v1, ctypes.byref(qs), M,
+                              ctypes.c_void_p(hist.data_ptr()), st)
+        elif ndim == 2:
+            name = "ft_lattice2d"
+            rc = L.ft_lattice2d(ctypes.byref(win), H, shape[1], v0, v1, ctypes.byref(qs), M, int(maxes),
+                                ctypes.c_void_p(hist.data_ptr()), st)
+        else:
+            name = "ft_lattice3d"
+            rc = L.ft_lattice3d(ctypes.byref(win), H, shape[1], shape[2], v0, v1, ctypes.byref(qs), M,
+                                ctypes.c_void_p(hist.data_ptr()), st)
     del keep
-    _lib.check(rc, f"ft_lattice{ndim}d")
+    _lib.check(rc, name)
     return hist
 
 
@@ -174,9 +199,10 @@ def launch_lines(x, shape, M, quant, rows=None, first=0, hist=None):
     if hist is None:
         hist = new_lines_hist(M, dev)
     win = _lib.ft_window(ctypes.c_void_p(x.data_ptr()), dtype_code(x), int(first), int(x.shape[0]), 1, 0)
-    qs, keep = device_struct(quant, dev)
-    rc = L.ft_lines3d(ctypes.byref(win), H, shape[1], shape[2], v0, v1, ctypes.byref(qs), M,
-                      ctypes.c_void_p(hist.data_ptr()), _stream_ptr(dev))
+    with on_device(dev):
+        qs, keep = device_struct(quant, dev)
+        rc = L.ft_lines3d(ctypes.byref(win), H, shape[1], shape[2], v0, v1, ctypes.byref(qs), M,
+                          ctypes.c_void_p(hist.data_ptr()), _stream_ptr(dev))
     del keep
     _lib.check(rc, "ft_lines3d")
     return hist
@@ -225,8 +251,9 @@ def curves_from_rows(hist, M, row_w):
     w = _row_weights(row_w, dev)
     n_desc = w.shape[0]
     out = t.empty((n_desc, M + 1) if batch == 1 else (batch, n_desc, M + 1), dtype=t.int64, device=dev)
-    rc = L.ft_curves(ctypes.c_void_p(hist.data_ptr()), n_rows, M, batch, n_desc, ctypes.c_void_p(w.data_ptr()),
-                     ctypes.c_void_p(out.data_ptr()), _stream_ptr(dev))
+    with on_device(dev):
+        rc = L.ft_curves(ctypes.c_void_p(hist.data_ptr()), n_rows, M, batch, n_desc,
+                         ctypes.c_void_p(w.data_ptr()), ctypes.c_void_p(out.data_ptr()), _stream_ptr(dev))
     _lib.check(rc, "ft_curves")
     return out
 
@@ -257,8 +284,9 @@ def finalize(ndim, M, hist, maps=True, tables=()):
         cw = t.from_numpy(np.stack([class_weights(ndim, w) for w in tables])).to(dev)
         num = t.empty((n_desc, M + 1) if batch == 1 else (batch, n_desc, M + 1), dtype=t.int64, device=dev)
     ptr = lambda a: ctypes.c_void_p(a.data_ptr()) if a is not None else None  # noqa: E731
-    rc = L.ft_finalize(ndim, M, batch, ptr(hist), ptr(q_in), ptr(q_out), n_desc, ptr(cw), ptr(num),
-                       _stream_ptr(dev))
+    with on_device(dev):
+        rc = L.ft_finalize(ndim, M, batch, ptr(hist), ptr(q_in), ptr(q_out), n_desc, ptr(cw), ptr(num),
+                           _stream_ptr(dev))
     _lib.check(rc, "ft_finalize")
     return q_in, q_out, num
 
@@ -274,8 +302,9 @@ def curves_from_maps(q_in, q_out, M, eighths_list, device):
     r = t.from_numpy(np.ascontiguousarray(rows)).to(device)
     rw = t.from_numpy(np.ascontiguousarray(row_w)).to(device)
     out = t.empty((len(w), M + 1), dtype=t.int64, device=device)
-    rc = L.ft_curves(ctypes.c_void_p(r.data_ptr()), rows.shape[0], M, 1, len(w), ctypes.c_void_p(rw.data_ptr()),
-                     ctypes.c_void_p(out.data_ptr()), _stream_ptr(device))
+    with on_device(device):
+        rc = L.ft_curves(ctypes.c_void_p(r.data_ptr()), rows.shape[0], M, 1, len(w),
+                         ctypes.c_void_p(rw.data_ptr()), ctypes.c_void_p(out.data_ptr()), _stream_ptr(device))
     _lib.check(rc, "ft_curves")
     return out.cpu().numpy()
 
@@ -285,9 +314,10 @@ def quantize_device(x, quant, M):
     t = torch()
     L = _lib.load()
     out = t.empty(x.shape, dtype=t.int32, device=x.device)
-    qs, keep = device_struct(quant, x.device, f64=x.dtype == t.float64)
-    rc = L.ft_quantize(ctypes.c_void_p(x.data_ptr()), dtype_code(x), x.numel(), ctypes.byref(qs), M,
-                       ctypes.c_void_p(out.data_ptr()), _stream_ptr(x.device))
+    with on_device(x.device):
+        qs, keep = device_struct(quant, x.device, f64=x.dtype == t.float64)
+        rc = L.ft_quantize(ctypes.c_void_p(x.data_ptr()), dtype_code(x), x.numel(), ctypes.byref(qs), M,
+                           ctypes.c_void_p(out.data_ptr()), _stream_ptr(x.device))
     del keep
     _lib.check(rc, "ft_quantize")
     return out
@@ -299,8 +329,9 @@ def minmax_device(x):
     L = _lib.load()
     out = t.empty(4, dtype=t.int32, device=x.device)
     code = dtype_code(x)
-    rc = L.ft_minmax(ctypes.c_void_p(x.data_ptr()), code, x.numel(), ctypes.c_void_p(out.data_ptr()),
-                     _stream_ptr(x.device))
+    with on_device(x.device):
+        rc = L.ft_minmax(ctypes.c_void_p(x.data_ptr()), code, x.numel(), ctypes.c_void_p(out.data_ptr()),
+                         _stream_ptr(x.device))
     _lib.check(rc, "ft_minmax")
     raw = out.cpu().numpy()
     if code == _lib.FT_F64:

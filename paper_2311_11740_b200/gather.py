@@ -68,6 +68,8 @@ def _torch_dtype(np_dtype):
 
 def resident_hist(src, ndim, device, rows, workers=1, hist=None, kind=MAP):
     x, quant = src.device_field(device)
+    if x.device != device:
+        raise ValueError(f"the source's field lives on {x.device}, not on {device}")
     if hist is None:
         hist = kind.new(ndim, src.max_level, device)
     v0, v1 = rows
@@ -78,6 +80,11 @@ def resident_hist(src, ndim, device, rows, workers=1, hist=None, kind=MAP):
 
 def stream_hist(src, ndim, device, rows, chunk_bytes=DEFAULT_CHUNK_BYTES, hist=None, kind=MAP):
     """Double-buffered pinned-host -> HBM streaming of a source's rows/planes."""
+    with engine.on_device(device):  # streams and events belong to ``device``
+        return _stream_hist(src, ndim, device, rows, chunk_bytes, hist, kind)
+
+
+def _stream_hist(src, ndim, device, rows, chunk_bytes, hist, kind):
     t = engine.torch()
     H = src.height
     M = src.max_level
@@ -127,7 +134,10 @@ def stream_hist(src, ndim, device, rows, chunk_bytes=DEFAULT_CHUNK_BYTES, hist=N
 
 def source_hist(src, ndim, device=None, workers=1, rows=None, chunk_bytes=DEFAULT_CHUNK_BYTES, kind=MAP):
     """Histogram of ``src`` for vertex rows ``rows`` on one GPU."""
-    dev = engine.default_device(device)
+    if device is None and src.mode == "device":
+        dev = src.tensor.device  # a resident field is processed where it lives
+    else:
+        dev = engine.default_device(device)
     rows = rows if rows is not None else (0, src.height + 1)
     if src.mode in ("in-memory", "device"):
         return resident_hist(src, ndim, dev, rows, workers, kind=kind)

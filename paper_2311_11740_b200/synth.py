@@ -94,3 +94,75 @@ def grf_2d(shape, sigma, seed, device):
     _smooth_axis_(torch, x, w, min(r, (W - 1) // 2), 1, t)
     _smooth_axis_(torch, t, w, min(r, (H - 1) // 2), 0, x)
     return x
+
+
+# --------------------------------------------------------------------------
+# BASELINE.json configs (shared by bench.py, tools/prof_run.py and the
+# config-scale parity tests, tests/test_gpu_configs.py)
+
+CONFIG_NAMES = ("c1", "c2", "c3", "c4a", "c4b", "c5")
+
+
+def config_field(name, device, seed=2311, planes=None):
+    """The synthetic input of BASELINE config ``name`` on ``device``.
+
+    Returns a dict: ``x`` (CUDA tensor: float32 samples, or uint8 / uint16
+    raw values), ``M`` (max level), ``value_range`` ((lo, hi) for
+    quantize_with_range, or None for identity levels), ``shape`` (the global
+    field shape; for C3 the image shape), ``batch`` (images, C3 only).
+    ``planes`` = (p0, p1) builds only those planes of the 3D f32 configs
+    (bit-identical to the same planes of the whole field; C5 slabs)."""
+    import torch
+
+    if name == "c1":  # 256^2 i.i.d. Uniform[0,1), 100 levels on [0, 1]
+        g = torch.Generator(device="cpu")
+        g.manual_seed(seed)
+        x = torch.rand((256, 256), generator=g, dtype=torch.float32).to(device)
+        return dict(x=x, M=99, value_range=(0.0, 1.0), shape=(256, 256), batch=1)
+    if name == "c2":  # 8192^2 GRF sigma 4 px, min-max to [0, 1], 256 levels
+        x = grf_2d((8192, 8192), 4.0, seed, device)
+        normalise_(x, x.min(), x.max())
+        return dict(x=x, M=255, value_range=(0.0, 1.0), shape=(8192, 8192), batch=1)
+    if name == "c3":  # 512 u8 images 1024^2, sigma ~ U[1, 8] px, quantised to 0..255
+        n, shape = 512, (1024, 1024)
+        sig = np.random.default_rng(seed).uniform(1.0, 8.0, n)
+        x = torch.empty((n,) + shape, dtype=torch.uint8, device=device)
+        for b in range(n):
+            im = grf_2d(shape, float(sig[b]), seed + b, device)
+            im = (im - im.min()) / (im.max() - im.min())
+            x[b] = torch.floor(im * 255 + 0.5).to(torch.uint8)
+        return dict(x=x, M=255, value_range=None, shape=shape, batch=n)
+    if name in ("c4a", "c5"):
+        shape, sigma, M = {"c4a": ((512, 512, 512), 3.0, 255), "c5": ((2048, 2048, 2048), 4.0, 511)}[name]
+        p0, p1 = planes if planes is not None else (0, shape[0])
+        x = grf_slab(shape, sigma, seed, (p0, p1), device)
+        if planes is None:
+            lo, hi = x.min(), x.max()
+        else:  # the global extrema (needs the whole field once; cached per process)
+            lo, hi = _global_extrema(shape, sigma, seed, device)
+        normalise_(x, lo, hi)
+        return dict(x=x, M=M, value_range=(0.0, 1.0), shape=shape, batch=1)
+    if name == "c4b":  # 1024 x 1024 x 256 u16 cube (sigma 3), quantize(raw, 1023) auto-range
+        shape = (1024, 1024, 256)
+        x = grf_slab(shape, 3.0, seed, (0, shape[0]), device)
+        normalise_(x, x.min(), x.max())
+        x = torch.floor(x * 65535 + 0.5).to(torch.int32).to(torch.uint16)
+        return dict(x=x, M=1023, value_range="auto", shape=shape, batch=1)
+    raise ValueError(f"unknown config {name!r}")
+
+
+_EXTREMA = {}
+
+
+def _global_extrema(shape, sigma, seed, device, chunk=256):
+    key = (tuple(shape), float(sigma), int(seed))
+    if key not in _EXTREMA:
+        lo = hi = None
+        for p0 in range(0, shape[0], chunk):
+            s = grf_slab(shape, sigma, seed, (p0, min(p0 + chunk, shape[0])), device)
+            a, b = s.min(), s.max()
+            lo = a if lo is None else min(lo, a)
+            hi = b if hi is None else max(hi, b)
+            del s
+        _EXTREMA[key] = (lo, hi)
+    return _EXTREMA[key]

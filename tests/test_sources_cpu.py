@@ -41,3 +41,33 @@ def test_stream_source_size_mismatch(tmp_path):
     p = _write(tmp_path, np.zeros(59, np.float32))
     with pytest.raises(ValueError):
         RawVolumeSource(p, (4, 3, 5), "f32", 255, value_range=(0.0, 1.0))
+
+
+def test_read_pencil_returns_decoded_levels_identity(tmp_path):
+    # reference RawVolumeSource.read_pencil (sources.py:379-386) returns int32
+    # levels, never the raw bytes
+    vol = np.random.default_rng(1).integers(0, 256, size=(3, 4, 5)).astype(np.uint8)
+    p = _write(tmp_path, vol)
+    with ft.open_raw_lowmem(p, (4, 3, 5)) as src:
+        pen = src.read_pencil(2, 1)
+        assert pen.dtype == np.int32 and np.array_equal(pen, vol[2, 1].astype(np.int32))
+
+
+def test_array_source_range_checks_identity_levels(tmp_path):
+    # identity levels outside [0, M] raise like Field2D/3D (fields.py:48-59)
+    ok = np.random.default_rng(2).integers(0, 8, size=(4, 5, 6)).astype(np.int32)
+    ft.ArraySource(ok, 7)
+    for bad in (ok + 1, ok - 1):
+        with pytest.raises(ValueError, match=r"levels must lie in \[0, 7\]"):
+            ft.ArraySource(bad, 7)
+    with pytest.raises(ValueError):
+        ft.ArraySource(np.full((3, 3), 9, np.uint8), 7)
+    # memmaps are checked chunk by chunk as the engine stages them
+    path = tmp_path / "m.i32"
+    (ok + 1).tofile(path)
+    mm = np.memmap(path, dtype=np.int32, mode="r", shape=ok.shape)
+    src = ft.ArraySource(mm, 7)
+    out = np.empty((2,) + ok.shape[1:], np.int32)
+    with pytest.raises(ValueError):
+        src.read_rows(0, 2, out)
+    ft.ArraySource(np.full((3, 3), 2.5, np.float32), 7, value_range=(0.0, 8.0))  # samples: no check
