@@ -176,6 +176,15 @@ int ft_tables(int32_t ndim, int32_t *step, int32_t *src, int32_t *dst);
 int ft_quantize(const void *x, int32_t dtype, int64_t n, const ft_quant *q, int32_t M,
                 int32_t *out, void *stream);
 
+/* Verification hook (tests only, not a reference interface): run one of the
+ * three device quantizers the fused kernels inline -- path 0 to_level (map /
+ * wide kernels, ft_quantize), 1 to_level4 (march / lattice kernels, incl. the
+ * table-free FT_Q_POW2 form), 2 pack_pow2_sat (line kernels, float32 pairs,
+ * FT_Q_POW2 only, n even) -- over a flat float32 / uint16 buffer into int32
+ * levels, so every input value can be checked against fields.py:20-33. */
+int ft_quantize_probe(const void *x, int32_t dtype, int64_t n, const ft_quant *q, int32_t M, int32_t path,
+                      int32_t *out, void *stream);
+
 /* Device min / max of a buffer (quantize's data range, fields.py:44-45;
  * RawVolumeSource._scan_range, sources.py:335-347).  out: device uint32[2],
  * OVERWRITTEN with order-preserving keys of (min, max); decode with

@@ -7,7 +7,6 @@ or cannot be loaded, every entry point raises -- there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes
-import os
 import threading
 
 from . import build as _build
@@ -18,7 +17,7 @@ FT_Q_IDENTITY, FT_Q_TABLE, FT_Q_TABLE_ROBUST, FT_Q_POW2 = 0, 1, 2, 3
 FT_ERR_ARG, FT_ERR_CLASSIFY, FT_ERR_INTERNAL, FT_ERR_CUDA_BASE = 1, 2, 3, 1000
 
 EXPORTS = ("ft_hist2d", "ft_hist3d", "ft_lattice2d", "ft_lattice3d", "ft_lines3d", "ft_lines3d_ok", "ft_lines2d", "ft_lines2d_ok", "ft_finalize", "ft_curves", "ft_class_weights", "ft_tables",
-           "ft_quantize", "ft_minmax", "ft_key_to_double", "ft_key64_to_double", "ft_version")
+           "ft_quantize", "ft_quantize_probe", "ft_minmax", "ft_key_to_double", "ft_key64_to_double", "ft_version")
 
 
 class ft_quant(ctypes.Structure):
@@ -42,10 +41,6 @@ def load(build_if_missing=True):
         if _lib is not None:
             return _lib
         path = _build.LIB
-        override = os.environ.get("FT_LIB")  # A/B experiments with alternative builds
-        if override:
-            path = type(path)(override)
-            build_if_missing = False
         if build_if_missing and not _build.up_to_date():
             try:
                 _build.build()
@@ -71,6 +66,7 @@ def load(build_if_missing=True):
         L.ft_class_weights.argtypes = [i32, vp, vp]
         L.ft_tables.argtypes = [i32, vp, vp, vp]
         L.ft_quantize.argtypes = [vp, i32, i64, P(ft_quant), i32, vp, vp]
+        L.ft_quantize_probe.argtypes = [vp, i32, i64, P(ft_quant), i32, i32, vp, vp]
         L.ft_minmax.argtypes = [vp, i32, i64, vp, vp]
         L.ft_key_to_double.argtypes = [i32, ctypes.c_uint32]
         L.ft_key_to_double.restype = ctypes.c_double

@@ -66,7 +66,7 @@ def descriptor_curves_batch(images, max_level, tables, value_range=None, device=
     rw = [lattice.row_weights(2, tuple(int(e) for e in t.eighths)) for t in tables]
     if all(r is not None for r in rw) and engine.lattice_ok(2, (H, W), M):
         maxes = any(lattice.needs_max_rows(r[0]) for r in rw)
-        hist = engine.new_lattice_hist(2, M, dev, batch=N)
+        hist = engine.new_lattice_hist(2, M, dev, batch=N).view(N, 4, M + 2)  # batch axis kept for N == 1
         engine.launch_lattice(2, x, (H, W), M, quant, rows=(0, H + 1), hist=hist, batch=N, batch_stride=H * W,
                               maxes=maxes)
         num = engine.curves_from_rows(hist, M, np.array([r[0] for r in rw])).cpu().numpy()

@@ -4,26 +4,22 @@
 // (contrib3d.py:241-370).  Per vertex (i, j, k) the eight cells
 // (i-1+di, j-1+dj, k-1+dk) are keyed level*8 + slot (slot = di + 2dj + 4dk):
 // sorting the keys reproduces the reference's stable insertion argsort
-// exactly (ties resolve by slot).  Each sorted rank books ONE event into a
-// per-CTA shared-memory histogram keyed by the transition class
-// (type_n -> type_{n+1}, 40 classes) instead of the reference's
-// 15 q_in/q_out increments.  The classes of ranks 1-3 are a function of the
-// first four sorted slots and those of ranks 4-6 of the last four, so two
-// 4096-entry shared tables (one lookup each) classify all six middle ranks.
+// exactly (ties resolve by slot).  Each sorted rank books ONE event keyed by
+// the transition class (type_n -> type_{n+1}, 40 classes)
+// instead of the reference's 15 q_in/q_out increments.  The classes of ranks
+// 1-3 are a function of the first four sorted slots and those of ranks 4-6 of
+// the last four, so two 4096-entry tables (one lookup each) classify all six
+// middle ranks.
 //
-// Tiling: a 1024-thread CTA owns a 32 x 32 tile of vertex
-// columns (j, k) and marches vertex rows i (the slowest, slab axis).  Each
-// step stages one cell-plane tile (+1-cell low halo) into shared memory as
-// 16-bit levels, quantizing on the fly; the plane below stays in registers
-// as an already-sorted 4-key list, so a vertex sorts 4 new keys (5
-// compare-exchanges) and merges (9) instead of sorting 8 (19).  Global loads
-// run two planes ahead of the compute; tile addressing is 32-bit with the
-// per-tile bounds folded into a validity bit, so the per-plane cost is one
-// uniform 64-bit pointer bump.  Vertex columns j == W or k == D (the
-// high-side boundary) are done by a flat per-vertex kernel.
+// Two kernels:
+// * hist3d_march (default): a warp marches a strip of vertex rows along i
+//   (the slab axis) on packed 16-bit keys, two vertices per word, into a
+//   per-CTA shared-memory histogram -- M + 1 <= 8190 and the 40 x (M+2)
+//   histogram + tables in shared memory (M <= ~1150);
+// * hist3d_wide (any M the reference accepts, e.g. u16 identity levels):
+//   one vertex per thread, 32-bit keys, events booked straight into the
+//   global u64 histogram.
 #include <algorithm>
-#include <cstdlib>
-#include <cstring>
 
 #include "ft_common.cuh"
 #include "ft_lattice.cuh"
@@ -31,18 +27,12 @@
 
 namespace ft {
 
-constexpr int TJ3 = 32, TK3 = 32, NT3 = TJ3 * TK3;
-constexpr int PW3 = TK3 + 1;          // staged plane tile row pitch (33)
-constexpr int PN3 = (TJ3 + 1) * PW3;  // staged cells per plane (1089)
-constexpr int LD3 = (PN3 + NT3 - 1) / NT3;
-constexpr int PF3 = 2;                // planes in flight
 constexpr int NTAB = 4096;            // rank-group table entries
 
 struct Geo3 {
     int64_t H, W, D, v0, v1, first;
     int M;
-    int tiles_j, tiles_k, chunk;
-    int64_t n_items;
+    int tiles_j, tiles_k;
 };
 
 // Class ids of ranks (1,2,3) indexed by the first four sorted slots, and of
@@ -66,22 +56,6 @@ __device__ __forceinline__ uint32_t slot_index(uint32_t a, uint32_t b, uint32_t 
     return ((a & 7u) << 9) | ((b & 7u) << 6) | ((c & 7u) << 3) | (d & 7u);
 }
 
-// Book the 8 events of one vertex (k8 sorted ascending).
-__device__ __forceinline__ void book3(uint32_t* __restrict__ h, const uint32_t* __restrict__ ta,
-                                      const uint32_t* __restrict__ tb, const uint32_t (&k8)[8], uint32_t M2)
-{
-    const uint32_t ea = ta[slot_index(k8[0], k8[1], k8[2], k8[3])];
-    const uint32_t eb = tb[slot_index(k8[4], k8[5], k8[6], k8[7])];
-    atomicAdd(&h[k8[0] >> 3], 1u);
-    atomicAdd(&h[(ea & 0xFFu) * M2 + (k8[1] >> 3)], 1u);
-    atomicAdd(&h[((ea >> 8) & 0xFFu) * M2 + (k8[2] >> 3)], 1u);
-    atomicAdd(&h[(ea >> 16) * M2 + (k8[3] >> 3)], 1u);
-    atomicAdd(&h[(eb & 0xFFu) * M2 + (k8[4] >> 3)], 1u);
-    atomicAdd(&h[((eb >> 8) & 0xFFu) * M2 + (k8[5] >> 3)], 1u);
-    atomicAdd(&h[(eb >> 16) * M2 + (k8[6] >> 3)], 1u);
-    atomicAdd(&h[39u * M2 + (k8[7] >> 3)], 1u);
-}
-
 __device__ __forceinline__ void init_shared3(uint32_t* h, uint32_t* ta, uint32_t* tb, float* tt,
                                              const RankTables* __restrict__ rt, const QuantDev& q, int M2,
                                              bool table)
@@ -103,132 +77,7 @@ __device__ __forceinline__ void flush_hist(const uint32_t* h, unsigned long long
     }
 }
 
-template <int DT, int QM>
-__global__ void __launch_bounds__(NT3, 1) hist3d_tiled(const typename Elem<DT>::T* __restrict__ buf, Geo3 g,
-                                                       QuantDev q, const RankTables* __restrict__ rt,
-                                                       unsigned long long* __restrict__ hist)
-{
-    using T = typename Elem<DT>::T;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int M2 = g.M + 2;
-    uint32_t* h = reinterpret_cast<uint32_t*>(smem_raw);
-    uint32_t* ta = h + 40 * M2;
-    uint32_t* tb = ta + NTAB;
-    float* tt = reinterpret_cast<float*>(tb + NTAB);
-    uint16_t* pl = reinterpret_cast<uint16_t*>(tt + M2);
-    init_shared3(h, ta, tb, tt, rt, q, M2, QM != FT_Q_IDENTITY);
-    __syncthreads();
-
-    const int tid = threadIdx.x;
-    const int ty = tid / TK3, tx = tid % TK3;
-    const int64_t per_chunk = (int64_t)g.tiles_j * g.tiles_k;
-    const int64_t it0 = g.n_items * blockIdx.x / gridDim.x;
-    const int64_t it1 = g.n_items * (blockIdx.x + 1) / gridDim.x;
-    const uint32_t sentinel = (uint32_t)g.M + 1;
-    const int64_t plane_elems = g.W * g.D;
-    const int Wi = (int)g.W, Di = (int)g.D;
-
-    int lr[LD3], lc[LD3];
-#pragma unroll
-    for (int e = 0; e < LD3; ++e) {
-        const int idx = tid + e * NT3;
-        lr[e] = idx / PW3;
-        lc[e] = idx % PW3;
-    }
-
-    for (int64_t item = it0; item < it1; ++item) {
-        const int64_t ch = item / per_chunk;
-        const int rem = (int)(item - ch * per_chunk);
-        const int j0 = (rem / g.tiles_k) * TJ3;
-        const int k0 = (rem % g.tiles_k) * TK3;
-        const int64_t ia = g.v0 + ch * g.chunk;
-        const int64_t ib = min(ia + (int64_t)g.chunk, g.v1);
-        const bool active = (j0 + ty < Wi) && (k0 + tx < Di);
-
-        // per-tile load slots: in-plane offset + validity (fixed over the march)
-        int off[LD3];
-        bool ok[LD3];
-#pragma unroll
-        for (int e = 0; e < LD3; ++e) {
-            const int jj = j0 - 1 + lr[e], kk = k0 - 1 + lc[e];
-            ok[e] = (tid + e * NT3 < PN3) && jj >= 0 && jj < Wi && kk >= 0 && kk < Di;
-            off[e] = ok[e] ? jj * Di + kk : 0;
-        }
-        T lv[PF3 + 1][LD3];
-        auto fetch = [&](int64_t p, T (&dst)[LD3]) {
-            const bool pin = p >= 0 && p < g.H;
-            const T* base = buf + (pin ? (p - g.first) * plane_elems : 0);
-#pragma unroll
-            for (int e = 0; e < LD3; ++e) {
-                dst[e] = T(0);
-                if (pin && ok[e]) dst[e] = ld_stream(base + off[e]);
-            }
-        };
-        auto store = [&](int64_t p, uint16_t* dstp, const T (&src)[LD3]) {
-            const bool pin = p >= 0 && p < g.H;
-#pragma unroll
-            for (int e = 0; e < LD3; ++e) {
-                const int idx = tid + e * NT3;
-                if (idx < PN3)
-                    dstp[idx] = (uint16_t)((pin && ok[e])
-                                               ? to_level<DT, QM>(src[e], tt, q.scale, q.bias, q.negate, g.M)
-                                               : sentinel);
-            }
-        };
-        fetch(ia - 1, lv[0]);
-#pragma unroll
-        for (int s = 1; s <= PF3; ++s) fetch(ia - 1 + s, lv[s]);
-        store(ia - 1, pl, lv[0]);
-        __syncthreads();
-
-        const int c00 = ty * PW3 + tx;
-        uint32_t lo0 = (uint32_t)pl[c00] * 8 + 0;
-        uint32_t lo1 = (uint32_t)pl[c00 + PW3] * 8 + 2;
-        uint32_t lo2 = (uint32_t)pl[c00 + 1] * 8 + 4;
-        uint32_t lo3 = (uint32_t)pl[c00 + PW3 + 1] * 8 + 6;
-        sort4(lo0, lo1, lo2, lo3);
-
-        for (int64_t i = ia; i < ib; ++i) {
-            uint16_t* cur = pl + ((i - ia + 1) & 1) * PN3;
-            store(i, cur, lv[1]);
-#pragma unroll
-            for (int s = 1; s < PF3; ++s)
-#pragma unroll
-                for (int e = 0; e < LD3; ++e) lv[s][e] = lv[s + 1][e];
-            if (i + PF3 < ib) fetch(i + PF3, lv[PF3]);
-            __syncthreads();
-            uint32_t u0 = (uint32_t)cur[c00] * 8 + 1;
-            uint32_t u1 = (uint32_t)cur[c00 + PW3] * 8 + 3;
-            uint32_t u2 = (uint32_t)cur[c00 + 1] * 8 + 5;
-            uint32_t u3 = (uint32_t)cur[c00 + PW3 + 1] * 8 + 7;
-            sort4(u0, u1, u2, u3);
-            if (active) {
-                uint32_t k8[8] = {lo0, lo1, lo2, lo3, u0, u1, u2, u3};
-                merge44(k8);
-                book3(h, ta, tb, k8, (uint32_t)M2);
-            }
-            lo0 = u0 - 1;
-            lo1 = u1 - 1;
-            lo2 = u2 - 1;
-            lo3 = u3 - 1;
-        }
-        __syncthreads();
-    }
-    __syncthreads();
-    flush_hist(h, hist, 40 * M2);
-}
-
-// Same booking as hist3d_tiled with TWO k-adjacent vertices per thread: the
-// keys (level * 8 + slot <= 65535 for M + 1 <= 8190) of both vertices ride
-// in the 16-bit halves of one word, so the sort4 / merge44 networks run once
-// for the pair (VIMNMX.U16x2 min / max), the plane is read as aligned 32-bit
-// level pairs, and the per-plane barrier, loads and loop overhead serve twice
-// the vertices.  Tile 32 x 64 vertices (1024 threads).
-constexpr int TJP = 32, TKP = 64, NTP = TJP * TKP / 2;
-constexpr int PWP = TKP + 2;            // staged row pitch: cells k0-1 .. k0+64 (even)
-constexpr int PNP = (TJP + 1) * PWP;    // staged cells per plane
-constexpr int LDP = (PNP + NTP - 1) / NTP;
-
+// Two-vertex (packed 16-bit halves) compare-exchange networks: VIMNMX.U16x2.
 __device__ __forceinline__ void cswap2(uint32_t& a, uint32_t& b)
 {
     const uint32_t lo = __vminu2(a, b);
@@ -256,139 +105,8 @@ __device__ __forceinline__ void merge44x2(uint32_t* k)
     cswap2(k[5], k[6]);
 }
 
-template <int DT, int QM>
-__global__ void __launch_bounds__(NTP, 1) hist3d_pair(const typename Elem<DT>::T* __restrict__ buf, Geo3 g,
-                                                      QuantDev q, const RankTables* __restrict__ rt,
-                                                      unsigned long long* __restrict__ hist)
-{
-    using T = typename Elem<DT>::T;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int M2 = g.M + 2;
-    uint32_t* h = reinterpret_cast<uint32_t*>(smem_raw);
-    uint32_t* ta = h + 40 * M2;
-    uint32_t* tb = ta + NTAB;
-    float* tt = reinterpret_cast<float*>(tb + NTAB);
-    uint16_t* pl = reinterpret_cast<uint16_t*>(tt + ((M2 + 1) & ~1));  // 4-byte aligned
-    init_shared3(h, ta, tb, tt, rt, q, M2, QM != FT_Q_IDENTITY);
-    __syncthreads();
-
-    const int tid = threadIdx.x;
-    const int ty = tid / (TKP / 2), tx = tid % (TKP / 2);
-    const int64_t per_chunk = (int64_t)g.tiles_j * g.tiles_k;
-    const int64_t it0 = g.n_items * blockIdx.x / gridDim.x;
-    const int64_t it1 = g.n_items * (blockIdx.x + 1) / gridDim.x;
-    const uint32_t sentinel = (uint32_t)g.M + 1;
-    const int64_t plane_elems = g.W * g.D;
-    const int Wi = (int)g.W, Di = (int)g.D;
-    const int w0i = (ty * PWP + 2 * tx) / 2, w1i = w0i + PWP / 2;  // 32-bit words of rows j-1, j
-
-    int lr[LDP], lc[LDP];
-#pragma unroll
-    for (int e = 0; e < LDP; ++e) {
-        const int idx = tid + e * NTP;
-        lr[e] = idx / PWP;
-        lc[e] = idx % PWP;
-    }
-
-    for (int64_t item = it0; item < it1; ++item) {
-        const int64_t ch = item / per_chunk;
-        const int rem = (int)(item - ch * per_chunk);
-        const int j0 = (rem / g.tiles_k) * TJP;
-        const int k0 = (rem % g.tiles_k) * TKP;
-        const int64_t ia = g.v0 + ch * g.chunk;
-        const int64_t ib = min(ia + (int64_t)g.chunk, g.v1);
-        const bool act_lo = (j0 + ty < Wi) && (k0 + 2 * tx < Di);
-        const bool act_hi = (j0 + ty < Wi) && (k0 + 2 * tx + 1 < Di);
-
-        int off[LDP];
-        bool ok[LDP];
-#pragma unroll
-        for (int e = 0; e < LDP; ++e) {
-            const int jj = j0 - 1 + lr[e], kk = k0 - 1 + lc[e];
-            ok[e] = (tid + e * NTP < PNP) && jj >= 0 && jj < Wi && kk >= 0 && kk < Di;
-            off[e] = ok[e] ? jj * Di + kk : 0;
-        }
-        T lv[PF3 + 1][LDP];
-        auto fetch = [&](int64_t p, T (&dst)[LDP]) {
-            const bool pin = p >= 0 && p < g.H;
-            const T* base = buf + (pin ? (p - g.first) * plane_elems : 0);
-#pragma unroll
-            for (int e = 0; e < LDP; ++e) {
-                dst[e] = T(0);
-                if (pin && ok[e]) dst[e] = ld_stream(base + off[e]);
-            }
-        };
-        auto store = [&](int64_t p, uint16_t* dstp, const T (&src)[LDP]) {
-            const bool pin = p >= 0 && p < g.H;
-#pragma unroll
-            for (int e = 0; e < LDP; ++e) {
-                const int idx = tid + e * NTP;
-                if (idx < PNP)
-                    dstp[idx] = (uint16_t)((pin && ok[e])
-                                               ? to_level<DT, QM>(src[e], tt, q.scale, q.bias, q.negate, g.M)
-                                               : sentinel);
-            }
-        };
-        // packed keys of one staged plane: slots (dj, dk) = (0,0) (1,0) (0,1)
-        // (1,1) -> 0, 2, 4, 6 (+ di); low half = vertex k, high half = k+1
-        auto keys = [&](const uint16_t* plane, uint32_t di, uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d) {
-            const uint32_t* p32 = reinterpret_cast<const uint32_t*>(plane);
-            const uint32_t r0 = p32[w0i], r0n = p32[w0i + 1], r1 = p32[w1i], r1n = p32[w1i + 1];
-            a = r0 * 8u + di * 0x10001u;
-            b = r1 * 8u + (2u + di) * 0x10001u;
-            c = __byte_perm(r0, r0n, 0x5432) * 8u + (4u + di) * 0x10001u;
-            d = __byte_perm(r1, r1n, 0x5432) * 8u + (6u + di) * 0x10001u;
-            sort4x2(a, b, c, d);
-        };
-        fetch(ia - 1, lv[0]);
-#pragma unroll
-        for (int s = 1; s <= PF3; ++s) fetch(ia - 1 + s, lv[s]);
-        store(ia - 1, pl, lv[0]);
-        __syncthreads();
-        uint32_t lo0, lo1, lo2, lo3;
-        keys(pl, 0u, lo0, lo1, lo2, lo3);
-
-        for (int64_t i = ia; i < ib; ++i) {
-            uint16_t* cur = pl + ((i - ia + 1) & 1) * PNP;
-            store(i, cur, lv[1]);
-#pragma unroll
-            for (int s = 1; s < PF3; ++s)
-#pragma unroll
-                for (int e = 0; e < LDP; ++e) lv[s][e] = lv[s + 1][e];
-            if (i + PF3 < ib) fetch(i + PF3, lv[PF3]);
-            __syncthreads();
-            uint32_t u0, u1, u2, u3;
-            keys(cur, 1u, u0, u1, u2, u3);
-            if (act_lo || act_hi) {
-                uint32_t k8[8] = {lo0, lo1, lo2, lo3, u0, u1, u2, u3};
-                merge44x2(k8);
-                if (act_lo) {
-                    uint32_t kl[8];
-#pragma unroll
-                    for (int s = 0; s < 8; ++s) kl[s] = k8[s] & 0xFFFFu;
-                    book3(h, ta, tb, kl, (uint32_t)M2);
-                }
-                if (act_hi) {
-                    uint32_t kh[8];
-#pragma unroll
-                    for (int s = 0; s < 8; ++s) kh[s] = k8[s] >> 16;
-                    book3(h, ta, tb, kh, (uint32_t)M2);
-                }
-            }
-            lo0 = u0 - 0x10001u;
-            lo1 = u1 - 0x10001u;
-            lo2 = u2 - 0x10001u;
-            lo3 = u3 - 0x10001u;
-        }
-        __syncthreads();
-    }
-    __syncthreads();
-    flush_hist(h, hist, 40 * M2);
-}
-
 // ------------------------------------------------ register-march map kernel
-// The booking of hist3d_tiled / hist3d_pair on the register march of the line
-// kernels: a warp marches a strip of HMR vertex rows x 62 vertex columns
+// A warp marches a strip of HMR vertex rows x 62 vertex columns
 // along i; lane l holds the cells (kk, kk+1), kk = k0-1+2l, of HMR+1 cell rows
 // as packed level*8 words, so the keys (level*8 + slot) of its two vertices
 // share one word and sort4 / merge44 run once per pair (VIMNMX.U16x2); the
@@ -569,40 +287,41 @@ __global__ void __launch_bounds__(HM3_NTH, 1) hist3d_march(const typename Elem<D
     flush_hist(h, hist, 40 * M2);
 }
 
-// High-side boundary vertices (j == W, or k == D with j < W), flat.
+// Any level count: one vertex per thread (k fastest: coalesced cell loads,
+// the 8 neighbours of a vertex hit L1), 32-bit keys level*8 + slot, the
+// 8 events booked straight into the global u64 histogram (L2 atomics).  The
+// threshold table of a quantized input is read from global memory.
 template <int DT, int QM>
-__global__ void __launch_bounds__(256) hist3d_edge(const typename Elem<DT>::T* __restrict__ buf, Geo3 g,
+__global__ void __launch_bounds__(256) hist3d_wide(const typename Elem<DT>::T* __restrict__ buf, Geo3 g,
                                                    QuantDev q, const RankTables* __restrict__ rt,
                                                    unsigned long long* __restrict__ hist)
 {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int M2 = g.M + 2;
-    uint32_t* h = reinterpret_cast<uint32_t*>(smem_raw);
-    uint32_t* ta = h + 40 * M2;
-    uint32_t* tb = ta + NTAB;
-    float* tt = reinterpret_cast<float*>(tb + NTAB);
-    init_shared3(h, ta, tb, tt, rt, q, M2, QM != FT_Q_IDENTITY);
-    __syncthreads();
-    const int64_t per_row = (g.D + 1) + g.W;
-    const int64_t n = (g.v1 - g.v0) * per_row;
+    const uint64_t M2 = (uint64_t)g.M + 2;
+    const int64_t nj = g.W + 1, nk = g.D + 1;
+    const int64_t n = (g.v1 - g.v0) * nj * nk;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = g.v0 + t / per_row;
-        const int64_t r = t % per_row;
-        const int64_t j = r <= g.D ? g.W : r - (g.D + 1);
-        const int64_t k = r <= g.D ? r : g.D;
-        uint32_t k8[8];
+        const int64_t k = t % nk;
+        const int64_t r = t / nk;
+        const int64_t j = r % nj;
+        const int64_t i = g.v0 + r / nj;
+        uint32_t a[8];
 #pragma unroll
-        for (int s = 0; s < 8; ++s)
-            k8[s] = level3<DT, QM>(buf, g, i - 1 + (s & 1), j - 1 + ((s >> 1) & 1), k - 1 + ((s >> 2) & 1), tt, q) *
-                        8 + s;
-        uint32_t a[8] = {k8[0], k8[2], k8[4], k8[6], k8[1], k8[3], k8[5], k8[7]};
+        for (int s = 0; s < 8; ++s) {
+            // slot s = di + 2 dj + 4 dk (contrib3d.py:47-49); sorted in two
+            // groups of four (dk = 0 / 1) and merged
+            const int di = s & 1, dj = (s >> 1) & 1, dk = s >> 2;
+            a[(s & 3) + 4 * dk] = level3<DT, QM>(buf, g, i - 1 + di, j - 1 + dj, k - 1 + dk, q.tt, q) * 8u + s;
+        }
         sort4(a[0], a[1], a[2], a[3]);
         sort4(a[4], a[5], a[6], a[7]);
         merge44(a);
-        book3(h, ta, tb, a, (uint32_t)M2);
+        const uint32_t ea = rt->a[slot_index(a[0], a[1], a[2], a[3])];
+        const uint32_t eb = rt->b[slot_index(a[4], a[5], a[6], a[7])];
+        const uint32_t cls[8] = {0u, ea & 0xFFu, (ea >> 8) & 0xFFu, ea >> 16, eb & 0xFFu, (eb >> 8) & 0xFFu,
+                                 eb >> 16, 39u};
+#pragma unroll
+        for (int r8 = 0; r8 < 8; ++r8) atomicAdd(&hist[cls[r8] * M2 + (a[r8] >> 3)], 1ull);
     }
-    __syncthreads();
-    flush_hist(h, hist, 40 * M2);
 }
 
 // Rank-group tables from the step table: simulate the active-slot masks of
@@ -661,8 +380,9 @@ static const RankTables* device_rank_tables()
     return dev_tabs[dev];
 }
 
-size_t hist3d_smem(int M) { return (size_t)(40 * (M + 2) + 2 * NTAB + (M + 2)) * 4 + 2 * PN3 * 2; }
-size_t hist3d_pair_smem(int M) { return (size_t)(40 * (M + 2) + 2 * NTAB + ((M + 3) & ~1)) * 4 + 2 * PNP * 2; }
+// shared bytes of hist3d_march: the 40 x (M+2) histogram, both rank tables, the threshold table
+static size_t march3_smem(int M) { return (size_t)(40 * (M + 2) + 2 * NTAB + (M + 2)) * 4; }
+static bool march3_ok(int M) { return M + 1 <= 8190 && march3_smem(M) <= 227 * 1024; }
 
 template <int DT, int QM>
 static int launch3(const ft_window* win, int64_t H, int64_t W, int64_t D, int64_t v0, int64_t v1,
@@ -676,77 +396,29 @@ static int launch3(const ft_window* win, int64_t H, int64_t W, int64_t D, int64_
     g.H = H; g.W = W; g.D = D; g.v0 = v0; g.v1 = v1; g.first = win->first; g.M = M;
     QuantDev q{qa ? qa->mode : FT_Q_IDENTITY, qa ? qa->negate : 0, qa ? qa->scale : 0.f, qa ? qa->bias : 0.f,
                qa ? qa->thresholds : nullptr};
-    const int M2 = M + 2;
-    const size_t sm_edge = (size_t)(40 * M2 + 2 * NTAB + M2) * 4;
-    const size_t sm_tiled = hist3d_smem(M);
     auto* out = reinterpret_cast<unsigned long long*>(hist);
     const int nsm = sm_count();
-
-    static const char* which = getenv("FT_MAP3D");  // march (default) | pair | tiled (dev A/B)
-    const size_t sm_march = (size_t)(40 * M2 + 2 * NTAB + M2) * 4;
-    if ((!which || !strcmp(which, "march")) && sm_march <= 227 * 1024) {
-        // register march: every vertex (j, k) in [0, W] x [0, D], no edge kernel
+    if (march3_ok(M)) {
+        // register march: every vertex (j, k) in [0, W] x [0, D]
+        const size_t sm = march3_smem(M);
         const bool vec = D % 2 == 0 && reinterpret_cast<uintptr_t>(buf) % (2 * sizeof(T)) == 0;
         auto kern = vec ? hist3d_march<DT, QM, true> : hist3d_march<DT, QM, false>;
-        FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_march));
+        FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         int per_sm = 0;
-        FT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, HM3_NTH, sm_march));
-        if (per_sm < 1) return FT_ERR_ARG;
+        FT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, HM3_NTH, sm));
+        if (per_sm < 1) return FT_ERR_INTERNAL;
         g.tiles_j = (int)cdiv(W + 1, (HM3_NTH / 32) * HMR);
         g.tiles_k = (int)((D + 1) / 62 + 1);  // tile t: vertex columns 62 t - 1 .. 62 t + 60
         const int64_t work = (int64_t)g.tiles_j * g.tiles_k * (v1 - v0);
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * per_sm, cdiv(work, 32)));
-        kern<<<grid, HM3_NTH, sm_march, st>>>(buf, g, q, rt, out);
+        kern<<<grid, HM3_NTH, sm, st>>>(buf, g, q, rt, out);
         FT_CUDA_TRY(cudaGetLastError());
         return FT_OK;
     }
-    if (W > 0 && D > 0 && !(which && !strcmp(which, "tiled")) && hist3d_pair_smem(M) <= 227 * 1024) {
-        auto kern = hist3d_pair<DT, QM>;
-        const size_t sm = hist3d_pair_smem(M);
-        FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        int per_sm = 0;
-        FT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NTP, sm));
-        if (per_sm < 1) return FT_ERR_ARG;
-        g.tiles_j = (int)cdiv(W, TJP);
-        g.tiles_k = (int)cdiv(D, TKP);
-        const int64_t tiles = (int64_t)g.tiles_j * g.tiles_k;
-        const int64_t rows = v1 - v0;
-        const int64_t grid_cap = (int64_t)nsm * per_sm;
-        int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>(cdiv(8 * grid_cap, tiles), rows / 32));
-        g.chunk = (int)cdiv(rows, nchunks);
-        nchunks = cdiv(rows, g.chunk);
-        g.n_items = tiles * nchunks;
-        const int grid = (int)std::min<int64_t>(grid_cap, g.n_items);
-        kern<<<grid, NTP, sm, st>>>(buf, g, q, rt, out);
-        FT_CUDA_TRY(cudaGetLastError());
-    } else if (W > 0 && D > 0) {
-        auto kern = hist3d_tiled<DT, QM>;
-        FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_tiled));
-        int per_sm = 0;
-        FT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT3, sm_tiled));
-        if (per_sm < 1) return FT_ERR_ARG;
-        g.tiles_j = (int)cdiv(W, TJ3);
-        g.tiles_k = (int)cdiv(D, TK3);
-        const int64_t tiles = (int64_t)g.tiles_j * g.tiles_k;
-        const int64_t rows = v1 - v0;
-        const int64_t grid_cap = (int64_t)nsm * per_sm;
-        // enough items to balance (>= ~8 per CTA) while keeping marches long
-        int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>(cdiv(8 * grid_cap, tiles), rows / 32));
-        g.chunk = (int)cdiv(rows, nchunks);
-        nchunks = cdiv(rows, g.chunk);
-        g.n_items = tiles * nchunks;
-        const int grid = (int)std::min<int64_t>(grid_cap, g.n_items);
-        kern<<<grid, NT3, sm_tiled, st>>>(buf, g, q, rt, out);
-        FT_CUDA_TRY(cudaGetLastError());
-    }
-    {
-        auto kern = hist3d_edge<DT, QM>;
-        FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_edge));
-        const int64_t n = (v1 - v0) * ((D + 1) + W);
-        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256 * 16), nsm));
-        kern<<<grid, 256, sm_edge, st>>>(buf, g, q, rt, out);
-        FT_CUDA_TRY(cudaGetLastError());
-    }
+    const int64_t n = (v1 - v0) * (W + 1) * (D + 1);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), (int64_t)nsm * 8));
+    hist3d_wide<DT, QM><<<grid, 256, 0, st>>>(buf, g, q, rt, out);
+    FT_CUDA_TRY(cudaGetLastError());
     return FT_OK;
 }
 
@@ -764,7 +436,7 @@ extern "C" int ft_hist3d(const ft_window* win, int64_t H, int64_t W, int64_t D, 
     const int64_t need_lo = std::max<int64_t>(v0 - 1, 0), need_hi = std::min<int64_t>(v1 - 1, H - 1);
     if (need_lo <= need_hi && (win->data == nullptr || need_lo < win->first || need_hi >= win->first + win->count))
         return FT_ERR_ARG;
-    if (hist3d_smem(M) > 227 * 1024 || M + 1 > 8190) return FT_ERR_ARG;
+    if (M > (1 << 28) - 2) return FT_ERR_ARG;  // keys level*8 + slot in 32 bits
     const int qm = effective_qmode(q);
     if (qm != FT_Q_IDENTITY && (!q->thresholds || win->dtype == FT_I32)) return FT_ERR_ARG;
     cudaStream_t st = static_cast<cudaStream_t>(stream);

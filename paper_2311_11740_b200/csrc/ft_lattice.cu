@@ -156,187 +156,23 @@ __global__ void __launch_bounds__(LNT) lattice3d_kernel(const typename Elem<DT>:
     flush_rows<CP>(reinterpret_cast<uint32_t*>(h), hist, 4, M2, hs / 4, false);
 }
 
-// ------------------------------------------------ 3D, per-cell signatures
-// Same histograms with 5 instead of 8 shared atomics per lattice point
-// (profiles/r01/lattice_notes.md: the event ATOMS bound the kernel).  The
-// cube and its faces are booked ONCE per cell: a face appears at the level of
-// whichever of its two cells activates first, so under the reference's total
-// order -- level, then (k, j, i) lexicographic, the slot order of
-// contrib3d.py:47-49 -- every face is owned by exactly one cell, and cell c
-// contributes (1 cube, f faces) at its own level, f = #face neighbours that
-// activate after c.  One increment of signature row u = 6 - f at level(c)
-// replaces the cube event and three face events; the flush folds the seven
-// signature rows into C = sum_u sig_u and F = sum_u (6 - u) sig_u.  Edges and
-// vertices stay min-filter events.  Cells of plane i are signed one step late
-// (their +i neighbour arrives with plane i+1), so every slab/chunk covering
-// lattice rows [a, b) signs cell planes [a-1, b-1): disjoint and complete.
-// Tile: 1024 threads stage 32 x 32 words; 30 x 30 threads compute (lane 30
-// only forwards its word to lane 29 by shuffle for the +k neighbour).
-constexpr int SNT = 512;   // threads = staged words (16 rows x 32 words)
-constexpr int SCJ = 14;    // compute rows
-constexpr int SCW = 30;    // compute words per row (60 lattice columns)
-
-template <int DT, int QM, bool VEC>
-__global__ void __launch_bounds__(SNT, 4) lattice3d_sig_kernel(const typename Elem<DT>::T* __restrict__ buf, LGeo g,
-                                                               QuantDev q, unsigned long long* __restrict__ hist)
-{
-    using P2 = typename Pair<DT>::T;
-    using T = typename Elem<DT>::T;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int M2 = g.M + 2;
-    const int hs = g.hs;                                   // bytes per histogram row
-    char* h = reinterpret_cast<char*>(smem_raw);           // rows: sig u = 0..6, edges, vertices
-    float* tt = reinterpret_cast<float*>(h + 9 * hs);
-    uint32_t* pl = reinterpret_cast<uint32_t*>(tt + M2);   // [2][SNT] staged words
-    for (int i = threadIdx.x; i < 9 * hs / 4; i += SNT) reinterpret_cast<uint32_t*>(h)[i] = 0;
-    if (QM != FT_Q_IDENTITY && QM != FT_Q_POW2)
-        for (int i = threadIdx.x; i < M2; i += SNT) tt[i] = q.tt[i];
-    __syncthreads();
-    char* hsig = h;
-    char* hE = h + 7 * hs;
-    char* hV = h + 8 * hs;
-
-    const int tid = threadIdx.x;
-    const int ty = tid / 32, tx = tid % 32;
-    const bool warp_on = ty < SCJ;             // warp-uniform
-    const bool computes = warp_on && tx < SCW;
-    const int Wi = (int)g.W, Di = (int)g.D;
-    const int64_t plane_elems = g.W * g.D;
-    const uint32_t sent4 = (uint32_t)(g.M + 1) * 4u;
-    const uint32_t hs_pk = (uint32_t)hs;       // IMAD multiplier (u * hs per 16-bit half)
-    const int64_t per_chunk = (int64_t)g.tiles_j * g.tiles_k;
-    const int64_t it0 = g.n_items * blockIdx.x / gridDim.x;
-    const int64_t it1 = g.n_items * (blockIdx.x + 1) / gridDim.x;
-    const int cw = (ty + 1) * 32 + tx + 1;     // staged word this thread computes
-
-    for (int64_t item = it0; item < it1; ++item) {
-        const int64_t ch = item / per_chunk;
-        const int rem = (int)(item - ch * per_chunk);
-        const int j0 = (rem / g.tiles_k) * SCJ;
-        const int k0 = (rem % g.tiles_k) * (2 * SCW);
-        const int64_t ia = g.v0 + ch * g.chunk;
-        const int64_t ib = min(ia + (int64_t)g.chunk, g.v1);
-
-        const int jj = j0 - 1 + ty, kk = k0 - 2 + 2 * tx;
-        const bool row_ok = jj >= 0 && jj < Wi && kk >= 0;
-        const bool okx = row_ok && kk < Di, oky = row_ok && kk + 1 < Di;
-        // planes relative to ia-1: t = -1 .. n+1 (plane ia-1+t), valid iff t_lo <= t < t_hi
-        const int n = (int)(ib - ia);
-        const int t_lo = (int)max((int64_t)-1, 1 - ia);
-        const int t_hi = (int)min((int64_t)(n + 2), g.H - ia + 1);
-        const T* ptr = buf + ((ia - 2 - g.first) * plane_elems + (okx ? (int64_t)jj * Di + kk : 0));
-        auto fetch = [&](int t, const T* at) {
-            const bool pin = t >= t_lo && t < t_hi;
-            return load_pair<DT, VEC>(at, pin && okx, pin && oky);
-        };
-        auto store = [&](int t, uint32_t* dstp, const P2& v) {
-            const bool pin = t >= t_lo && t < t_hi;
-            dstp[tid] = pack_pair<DT, QM, 0>(v, pin && okx, pin && oky, tt, q, g.M, sent4);
-        };
-        // prologue: plane ia-2 (only its word at cw is needed) and plane ia-1
-        P2 ra = fetch(-1, ptr);
-        store(-1, pl, ra);
-        ra = fetch(0, ptr + plane_elems);
-        __syncthreads();
-        uint32_t ppW = pl[cw];
-        __syncthreads();
-        store(0, pl, ra);
-        ra = fetch(1, ptr + 2 * plane_elems);
-        P2 rb = fetch(2, ptr + 3 * plane_elems);
-        ptr += 4 * plane_elems;  // next fetch: t = 3
-        __syncthreads();
-
-        uint32_t pW = 0, pU = 0, pD = 0, pWm = 0, pWp = 0, pm2k = 0, pm2j = 0, pm4i = 0;
-        if (warp_on) {
-            pW = pl[cw];
-            pU = pl[cw - 32];
-            pD = pl[cw + 32];
-            const uint32_t WR = __shfl_down_sync(0xFFFFFFFFu, pW, 1);
-            pWm = shift_pair(pl[cw - 1], pW);
-            pWp = shift_pair(pW, WR);
-            pm2k = vmin2(pW, pWm);
-            pm2j = vmin2(pW, pU);
-            pm4i = vmin2(pm2k, vmin2(pU, shift_pair(pl[cw - 33], pU)));
-        }
-
-        auto step = [&](const uint32_t* cur) {
-            if (!warp_on) return;
-            const uint32_t W_ = cur[cw];
-            const uint32_t WR = __shfl_down_sync(0xFFFFFFFFu, W_, 1);
-            if (!computes) return;
-            const uint32_t U = cur[cw - 32];
-            const uint32_t D = cur[cw + 32];
-            const uint32_t Wm = shift_pair(cur[cw - 1], W_);
-            const uint32_t Um = shift_pair(cur[cw - 33], U);
-            const uint32_t m2k = vmin2(W_, Wm);             // face normal k
-            const uint32_t m2j = vmin2(W_, U);              // face normal j
-            const uint32_t m4i = vmin2(m2k, vmin2(U, Um));  // edge along i
-            inc2(hE, 0, hs, m4i);
-            inc2(hE, 0, hs, vmin2(m2k, pm2k));  // edge along j
-            inc2(hE, 0, hs, vmin2(m2j, pm2j));  // edge along k
-            inc2(hV, 0, hs, vmin2(m4i, pm4i));  // vertex
-            // signature of the plane-(i-1) cells pW: bit 15 / 31 of c' - n + k
-            // is "n activates before c" (k = 0 for -side n, -1 for +side n)
-            const uint32_t cb = pW | 0x80008000u;
-            const uint32_t r0 = cb - ppW;                 // -i
-            const uint32_t r1 = cb - pU;                  // -j
-            const uint32_t r2 = cb - pWm;                 // -k
-            const uint32_t r3 = cb - W_ - 0x10001u;       // +i
-            const uint32_t r4 = cb - pD - 0x10001u;       // +j
-            const uint32_t r5 = cb - pWp - 0x10001u;      // +k
-            const uint32_t u = ((r0 >> 15) & 0x10001u) + ((r1 >> 15) & 0x10001u) + ((r2 >> 15) & 0x10001u) +
-                               ((r3 >> 15) & 0x10001u) + ((r4 >> 15) & 0x10001u) + ((r5 >> 15) & 0x10001u);
-            inc2(hsig, 0, hs, u * hs_pk + pW);             // row u = 6 - f, at level(c)
-            ppW = pW;
-            pW = W_;
-            pU = U;
-            pD = D;
-            pWm = Wm;
-            pWp = shift_pair(W_, WR);
-            pm2k = m2k;
-            pm2j = m2j;
-            pm4i = m4i;
-        };
-        for (int s = 0; s < n; s += 2) {
-            uint32_t* cur = pl + SNT;  // step s: plane t = s+1 -> buffer 1
-            store(s + 1, cur, ra);
-            if (s + 2 < n) ra = fetch(s + 3, ptr);
-            ptr += plane_elems;
-            __syncthreads();
-            step(cur);
-            if (s + 1 >= n) break;
-            cur = pl;  // step s+1: plane t = s+2 -> buffer 0
-            store(s + 2, cur, rb);
-            if (s + 3 < n) rb = fetch(s + 4, ptr);
-            ptr += plane_elems;
-            __syncthreads();
-            step(cur);
-        }
-        __syncthreads();
-    }
-    __syncthreads();
-    // fold the signature rows into (cells, faces, edges, vertices)
-    const uint32_t* hw = reinterpret_cast<const uint32_t*>(h);
-    const int rw = hs / 4;
-    for (int l = threadIdx.x; l < M2; l += SNT) {
-        uint32_t c = 0, f = 0;
-#pragma unroll
-        for (int u = 0; u < 7; ++u) {
-            const uint32_t v = hw[u * rw + l];
-            c += v;
-            f += (6 - u) * v;
-        }
-        const uint32_t e = hw[7 * rw + l], x = hw[8 * rw + l];
-        if (c) atomicAdd(&hist[l], (unsigned long long)c);
-        if (f) atomicAdd(&hist[M2 + l], (unsigned long long)f);
-        if (e) atomicAdd(&hist[2 * M2 + l], (unsigned long long)e);
-        if (x) atomicAdd(&hist[3 * M2 + l], (unsigned long long)x);
-    }
-}
+// ------------------------------------------------ per-cell signatures
+// The cube and its faces are booked ONCE per cell: a face appears at the
+// level of whichever of its two cells activates first, so under the
+// reference's total order -- level, then (k, j, i) lexicographic, the slot
+// order of contrib3d.py:47-49 -- every face is owned by exactly one cell, and
+// cell c contributes (1 cube, f faces) at its own level, f = #face
+// neighbours that activate after c.  One increment of signature row u = 6 - f
+// at level(c) replaces the cube event and three face events; the flush folds
+// the seven signature rows into C = sum_u sig_u and F = sum_u (6 - u) sig_u.
+// Edges and vertices stay min-filter events.  Cells of plane i are signed one
+// step late (their +i neighbour arrives with plane i+1), so every slab/chunk
+// covering lattice rows [a, b) signs cell planes [a-1, b-1): disjoint and
+// complete.
 
 // --------------------------------- 3D, register-blocked and barrier-free
-// The same booking as lattice3d_sig_kernel (5 shared atomics per lattice
-// point) without staging: every WARP independently owns a strip of R lattice
+// The per-cell signature booking (5 shared atomics per lattice point)
+// without staging: every WARP independently owns a strip of R lattice
 // rows x 60 lattice columns and marches the planes.  Lane l holds the words
 // (two k-adjacent cells) of column pair l for the R+2 cell rows j0-1 .. j0+R
 // of the current plane in registers, so j-neighbours are registers and
@@ -459,7 +295,7 @@ __global__ void __launch_bounds__(256, 2) lattice3d_rb_kernel(const typename Ele
                 ev[r][1] = vmin2(m2k, pm2k[r]);  // edge along j
                 ev[r][2] = vmin2(m2j, pm2j[r]);  // edge along k
                 ev[r][3] = vmin2(m4i, pm4i[r]);  // vertex
-                // signature of the plane-(i-1) cells of row r (see lattice3d_sig_kernel).
+                // signature of the plane-(i-1) cells of row r (per-cell signatures, above).
                 // Each term is bit 15 / 31 of c' - n + k: "n activates before c".
                 // The -i term is the complement of the previous step's +i term and
                 // the -j term (rows >= 2) the complement of row r-1's +j term.
@@ -782,29 +618,6 @@ __global__ void __launch_bounds__(64) lattice2d_rb_kernel(const typename Elem<DT
 }
 
 
-// Privatisation degree: as many copies (8, 4 or 1) as keep the 16-bit packed
-// byte offsets in range and the 4 histogram rows within ~72 KB, so three
-// 512-thread CTAs still fit an SM.
-static int copies_for(int M)
-{
-    // Measured (profiles/r01/lattice_notes.md): with smooth fields the event
-    // levels of a warp are near-random mod 32, so splitting lanes into copy
-    // groups does not lower the conflict degree (2.5 wavefronts either way)
-    // while the larger footprint costs occupancy: 283 -> 257 Gvox/s at
-    // 2048^3.  Single copy unless FT_LATTICE_COPIES asks otherwise.
-    static const int forced = [] {
-        const char* e = getenv("FT_LATTICE_COPIES");
-        return e ? atoi(e) : 1;
-    }();
-    if (forced <= 1) return 1;
-    for (int cp : {8, 4, 2}) {
-        if (cp > forced) continue;
-        const int64_t bytes = (int64_t)(M + 2) * 4 * cp;
-        if ((int64_t)(M + 1) * 4 * cp + 4 * (cp - 1) <= 0xFFFF && 4 * bytes <= 72 * 1024) return cp;
-    }
-    return 1;
-}
-
 template <int DT, int QM>
 static int launch_l3(const ft_window* win, int64_t H, int64_t W, int64_t D, int64_t v0, int64_t v1,
                      const ft_quant* qa, int32_t M, uint64_t* hist, cudaStream_t st)
@@ -813,8 +626,7 @@ static int launch_l3(const ft_window* win, int64_t H, int64_t W, int64_t D, int6
     LGeo g{};
     g.H = H; g.W = W; g.D = D; g.v0 = v0; g.v1 = v1; g.first = win->first; g.M = M;
     const bool vec3 = D % 2 == 0 && reinterpret_cast<uintptr_t>(win->data) % 8 == 0;
-    static const char* which = getenv("FT_LATTICE_KERNEL");  // rb (default) | sig | staged
-    if ((!which || !strcmp(which, "rb")) && 6 * (((M + 2) * 4 + 15) / 16 * 16) + (M + 1) * 4 < 0xFFFF) {
+    if (6 * (((M + 2) * 4 + 15) / 16 * 16) + (M + 1) * 4 < 0xFFFF) {
         // R = 6 rows per warp strip: 127 registers, 2 CTAs/SM; measured at
         // 2048^3: R=4 451, R=6 479, R=8 384 (spills), R=4 forced to 3 CTAs 440 Gvox/s
         constexpr int R = 6, NTH = 256;
@@ -835,42 +647,13 @@ static int launch_l3(const ft_window* win, int64_t H, int64_t W, int64_t D, int6
         FT_CUDA_TRY(cudaGetLastError());
         return FT_OK;
     }
-    {
-        // per-cell signature kernel when its packed row offsets fit 16 bits
-        const int hs = ((M + 2) * 4 + 15) / 16 * 16;
-        // Measured at 2048^3 (profiles/r01/lattice_notes.md): 298 Gvox/s vs
-        // 308 for the 8-event kernel -- fewer ATOMS but more ALU and latency;
-        // opt-in until the barrier-free variant lands.
-        static const bool sig = which && !strcmp(which, "sig");
-        if (sig && 6 * hs + (M + 1) * 4 < 0xFFFF) {
-            g.hs = hs;
-            const size_t smem = (size_t)9 * hs + (size_t)(M + 2) * 4 + 2 * SNT * 4;
-            auto kern = vec3 ? lattice3d_sig_kernel<DT, QM, true> : lattice3d_sig_kernel<DT, QM, false>;
-            FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            int per_sm = 0;
-            FT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, SNT, smem));
-            if (per_sm < 1) return FT_ERR_ARG;
-            g.tiles_j = (int)cdiv(W + 1, SCJ);
-            g.tiles_k = (int)cdiv(D + 1, 2 * SCW);
-            const int64_t grid_cap = (int64_t)nsm_l() * per_sm;
-            plan_items(g, (int64_t)g.tiles_j * g.tiles_k, 1, grid_cap, 32);
-            const int grid = (int)std::min<int64_t>(grid_cap, g.n_items);
-            kern<<<grid, SNT, smem, st>>>(static_cast<const T*>(win->data), g, qdev(qa),
-                                          reinterpret_cast<unsigned long long*>(hist));
-            FT_CUDA_TRY(cudaGetLastError());
-            return FT_OK;
-        }
-    }
-    const int cp = copies_for(M);
-    g.hs = row_stride(M, cp);
+    // larger level counts: the staged kernel (one histogram copy; measured,
+    // profiles/r01/lattice_notes.md: privatised copies do not lower the
+    // conflict degree on smooth fields)
+    g.hs = row_stride(M, 1);
     const size_t smem = (size_t)4 * g.hs + (size_t)(M + 2) * 4 + 2 * LNT * 4;
     const bool vec = D % 2 == 0 && reinterpret_cast<uintptr_t>(win->data) % 8 == 0;
-    using K = void (*)(const T*, LGeo, QuantDev, unsigned long long*);
-    K kern;
-    if (vec) kern = cp == 8 ? lattice3d_kernel<DT, QM, true, 8> : cp == 4 ? lattice3d_kernel<DT, QM, true, 4>
-                  : cp == 2 ? lattice3d_kernel<DT, QM, true, 2> : lattice3d_kernel<DT, QM, true, 1>;
-    else kern = cp == 8 ? lattice3d_kernel<DT, QM, false, 8> : cp == 4 ? lattice3d_kernel<DT, QM, false, 4>
-              : cp == 2 ? lattice3d_kernel<DT, QM, false, 2> : lattice3d_kernel<DT, QM, false, 1>;
+    auto kern = vec ? lattice3d_kernel<DT, QM, true, 1> : lattice3d_kernel<DT, QM, false, 1>;
     FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     FT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, LNT, smem));
@@ -895,16 +678,13 @@ static int launch_l2(const ft_window* win, int64_t H, int64_t W, int64_t v0, int
     LGeo g{};
     g.H = H; g.W = W; g.D = 1; g.v0 = v0; g.v1 = v1; g.first = win->first; g.M = M;
     g.bstride = win->batch_stride;
-    // 2D: 8 copies only while they are small (many 256-thread CTAs per SM)
-    const int cp = (int64_t)(M + 2) * 4 * 8 * 4 <= 40 * 1024 ? 8 : 1;
-    g.hs = row_stride(M, cp);
+    g.hs = row_stride(M, 1);
     const int64_t batch = std::max<int64_t>(win->batch, 1);
     const size_t smem = (size_t)4 * g.hs + (size_t)(M + 2) * 4 + 2 * L2W * 4;
     const bool vec = W % 2 == 0 && (batch <= 1 || win->batch_stride % 2 == 0) &&
                      reinterpret_cast<uintptr_t>(win->data) % 8 == 0;
-    static const char* which = getenv("FT_LATTICE_KERNEL");  // rb (default) | staged
     const int hs_rb = ((M + 2) * 4 + 15) / 16 * 16;
-    if ((!which || !strcmp(which, "rb")) && 4 * hs_rb + (M + 1) * 4 < 0xFFFF) {
+    if (4 * hs_rb + (M + 1) * 4 < 0xFFFF) {
         g.hs = hs_rb;
         const size_t smem_rb = (size_t)7 * hs_rb + (size_t)(M + 2) * 4;
         using K = void (*)(const T*, LGeo, QuantDev, unsigned long long*);
@@ -929,15 +709,10 @@ static int launch_l2(const ft_window* win, int64_t H, int64_t W, int64_t v0, int
         FT_CUDA_TRY(cudaGetLastError());
         return FT_OK;
     }
+    // larger level counts: the staged kernel (one histogram copy)
     using K = void (*)(const T*, LGeo, QuantDev, unsigned long long*);
-    K kern;
-    if (maxes) {
-        if (vec) kern = cp == 8 ? lattice2d_kernel<DT, QM, true, true, 8> : lattice2d_kernel<DT, QM, true, true, 1>;
-        else kern = cp == 8 ? lattice2d_kernel<DT, QM, true, false, 8> : lattice2d_kernel<DT, QM, true, false, 1>;
-    } else {
-        if (vec) kern = cp == 8 ? lattice2d_kernel<DT, QM, false, true, 8> : lattice2d_kernel<DT, QM, false, true, 1>;
-        else kern = cp == 8 ? lattice2d_kernel<DT, QM, false, false, 8> : lattice2d_kernel<DT, QM, false, false, 1>;
-    }
+    K kern = maxes ? (vec ? lattice2d_kernel<DT, QM, true, true, 1> : lattice2d_kernel<DT, QM, true, false, 1>)
+                   : (vec ? lattice2d_kernel<DT, QM, false, true, 1> : lattice2d_kernel<DT, QM, false, false, 1>);
     FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     FT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L2W, smem));

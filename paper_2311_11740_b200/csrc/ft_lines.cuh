@@ -54,29 +54,13 @@ __device__ __forceinline__ uint32_t pack_pow2_sat(const typename Pair<DT>::T& v,
 // Packed level words carry the shared address of the block (LINES_SBASE, in
 // every half), so a half IS the shared address of a signature bin and the
 // plus/minus rows are an immediate above it: ATOMS [R + imm], no base add.
-#ifndef LINES_DEV_NOATOM
-#define LINES_DEV_NOATOM 0  // dev timing only (wrong results): bit 0 drops the dense, bit 1 the sparse ATOMS
-#endif
-#ifndef LINES_DEV_NOCONF
-#define LINES_DEV_NOCONF 0  // dev timing only (wrong results): bit 0 / 1: dense / sparse ATOMS without conflicts
-#endif
 template <int OFF>
 __device__ __forceinline__ void sinc2(uint32_t addr)
 {
     const uint32_t hi = __umulhi(addr, 0x10000u);
     const uint32_t lo = addr - hi * 0x10000u;
-    if constexpr ((LINES_DEV_NOATOM >> (OFF == 0 ? 0 : 1)) & 1) {
-        asm volatile("" ::"r"(lo), "r"(hi));
-    } else if constexpr ((LINES_DEV_NOCONF >> (OFF == 0 ? 0 : 1)) & 1) {
-        // conflict-free addresses (dense: lane-private words; sparse: one word)
-        asm volatile("" ::"r"(lo), "r"(hi));
-        const uint32_t a = OFF == 0 ? LINES_SBASE + (threadIdx.x & 31) * 4 : LINES_SBASE;
-        asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(a), "n"(OFF));
-        asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(a), "n"(OFF + 128));
-    } else {
-        asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(lo), "n"(OFF));
-        asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(hi), "n"(OFF));
-    }
+    asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(lo), "n"(OFF));
+    asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(hi), "n"(OFF));
 }
 // (a & m) | (b & ~m) as ONE LOP3 (left to itself ptxas sometimes splits it
 // into two around a hoisted b & ~m)

@@ -435,10 +435,7 @@ static bool lines_ok(int M)
 }
 
 
-#ifndef LINES_FUSED_DEF
-#define LINES_FUSED_DEF 1
-#endif
-// Interior and boundary items in one launch (MODE 2) or two (dev A/B)
+// Interior and boundary items in one launch (MODE 2)
 template <int DT, int QM, bool VEC, bool FOLD, int DS, int MODE>
 static int launch_lines_kernel(const ft_window* win, LGeo g, const QuantDev& qd, size_t smem, uint64_t* hist,
                                cudaStream_t st)
@@ -484,12 +481,7 @@ template <int DT, int QM, bool VEC, bool FOLD, int DS>
 static int launch_lines_two(const ft_window* win, const LGeo& g, const QuantDev& qd, size_t smem, uint64_t* hist,
                             cudaStream_t st)
 {
-    if constexpr (LINES_FUSED_DEF) {
-        return launch_lines_kernel<DT, QM, VEC, FOLD, DS, 2>(win, g, qd, smem, hist, st);
-    } else {
-        const int rc = launch_lines_kernel<DT, QM, VEC, FOLD, DS, 0>(win, g, qd, smem, hist, st);
-        return rc ? rc : launch_lines_kernel<DT, QM, VEC, FOLD, DS, 1>(win, g, qd, smem, hist, st);
-    }
+    return launch_lines_kernel<DT, QM, VEC, FOLD, DS, 2>(win, g, qd, smem, hist, st);
 }
 
 template <int DT, int QM, bool VEC, bool FOLD>

@@ -9,8 +9,7 @@ treats as uint64 (counts never exceed 2**63).
 from __future__ import annotations
 
 import ctypes
-import os as _os
-
+import warnings
 import numpy as np
 
 from . import _lib
@@ -87,7 +86,9 @@ def to_device(array, device, pinned=True):
         a = np.ascontiguousarray(array)
         if a.dtype == np.int64:
             a = a.astype(np.int32)
-        x = t.from_numpy(a)
+        with warnings.catch_warnings():  # read-only Field arrays: only ever read
+            warnings.simplefilter("ignore", UserWarning)
+            x = t.from_numpy(a)
         if pinned and x.numel() * x.element_size() >= (1 << 20):
             x = x.pin_memory()
     return x.to(device, non_blocking=True).contiguous()
@@ -124,13 +125,9 @@ def launch_hist(ndim, x, shape, M, quant, rows=None, first=0, hist=None, batch=1
 def _hist_call(L, ndim, win, H, shape, v0, v1, qs, M, hist, st):
     if ndim == 2:
         return L.ft_hist2d(ctypes.byref(win), H, shape[1], v0, v1, ctypes.byref(qs), M,
-                         ctypes.c_void_p(hist.data_ptr()), st)
-    else:
-        rc = L.ft_hist3d(ctypes.byref(win), H, shape[1], shape[2], v0, v1, ctypes.byref(qs), M,
-                         ctypes.c_void_p(hist.data_ptr()), st)
-    del keep
-    _lib.check(rc, f"ft_hist{ndim}d")
-    return hist
+                           ctypes.c_void_p(hist.data_ptr()), st)
+    return L.ft_hist3d(ctypes.byref(win), H, shape[1], shape[2], v0, v1, ctypes.byref(qs), M,
+                       ctypes.c_void_p(hist.data_ptr()), st)
 
 
 def new_lattice_hist(ndim, M, device, batch=1):
@@ -142,12 +139,8 @@ def _use_lines2d(kernel, batch):
     """ft_lines2d or ft_lattice2d for 2D rows 0..2.  ft_lines2d is the default:
     measured on B200 (ncu kernel durations, profiles/r01/lines2d_notes.md) it
     beats the lattice kernel on one large image (C2: 85 vs 90 us) and on
-    batches (C3: 715 vs 779 us).  ``kernel`` "lines" / "lattice" (or
-    FT_2D_KERNEL) forces one."""
-    force = kernel if kernel != "auto" else _os.environ.get("FT_2D_KERNEL", "auto")
-    if force in ("lines", "lattice"):
-        return force == "lines"
-    return True
+    batches (C3: 715 vs 779 us).  ``kernel`` "lines" / "lattice" forces one."""
+    return kernel != "lattice"
 
 
 def launch_lattice(ndim, x, shape, M, quant, rows=None, first=0, hist=None, batch=1, batch_stride=0,
@@ -250,7 +243,8 @@ def curves_from_rows(hist, M, row_w):
     n_rows = hist.shape[-2]
     w = _row_weights(row_w, dev)
     n_desc = w.shape[0]
-    out = t.empty((n_desc, M + 1) if batch == 1 else (batch, n_desc, M + 1), dtype=t.int64, device=dev)
+    # a batched (3D) histogram keeps its batch axis, also for one image
+    out = t.empty((n_desc, M + 1) if hist.dim() == 2 else (batch, n_desc, M + 1), dtype=t.int64, device=dev)
     with on_device(dev):
         rc = L.ft_curves(ctypes.c_void_p(hist.data_ptr()), n_rows, M, batch, n_desc,
                          ctypes.c_void_p(w.data_ptr()), ctypes.c_void_p(out.data_ptr()), _stream_ptr(dev))
@@ -275,14 +269,14 @@ def finalize(ndim, M, hist, maps=True, tables=()):
     dev = hist.device
     batch = hist.shape[0] if hist.dim() == 3 else 1
     T = NTYPE[ndim]
-    shp = (T, M + 2) if batch == 1 else (batch, T, M + 2)
+    shp = (T, M + 2) if hist.dim() == 2 else (batch, T, M + 2)
     q_in = t.empty(shp, dtype=t.int64, device=dev) if maps else None
     q_out = t.empty(shp, dtype=t.int64, device=dev) if maps else None
     n_desc = len(tables)
     cw = num = None
     if n_desc:
         cw = t.from_numpy(np.stack([class_weights(ndim, w) for w in tables])).to(dev)
-        num = t.empty((n_desc, M + 1) if batch == 1 else (batch, n_desc, M + 1), dtype=t.int64, device=dev)
+        num = t.empty((n_desc, M + 1) if hist.dim() == 2 else (batch, n_desc, M + 1), dtype=t.int64, device=dev)
     ptr = lambda a: ctypes.c_void_p(a.data_ptr()) if a is not None else None  # noqa: E731
     with on_device(dev):
         rc = L.ft_finalize(ndim, M, batch, ptr(hist), ptr(q_in), ptr(q_out), n_desc, ptr(cw), ptr(num),

@@ -40,13 +40,6 @@ def _plan(ft):
     return lattice.fused_plan(2, [t.eighths for t in _tabs(ft)])
 
 
-@pytest.fixture(autouse=True)
-def _lines2d_everywhere(monkeypatch):
-    """Route every 2D fused launch of this module to ft_lines2d (by default
-    only batches take it, engine._use_lines2d)."""
-    monkeypatch.setenv("FT_2D_KERNEL", "lines")
-
-
 def test_lines2d_golden(ft, golden):
     from paper_2311_11740_b200 import engine, lattice
     assert lattice.fused_plan(2, [t.eighths for t in _tabs(ft)])[1] is False  # no maxes: ft_lines2d
