@@ -10,9 +10,11 @@ _parallel.py:8-33) with:
   chunks of cell rows/planes in pinned host memory are copied to two device
   buffers on a side stream, so the H2D of chunk c+1 overlaps the kernel on
   chunk c.  Chunk c covers vertex rows [a, b) and holds cell rows
-  [a-2, b-1]; the low halo rows are simply re-sent.  A source that is
-  already a pinned torch tensor is copied straight from its own pages; any
-  other source is read into two pinned staging buffers first;
+  [a-2, b-1]; the two low halo rows are carried over from the previous
+  chunk's buffer device-to-device, so every row crosses PCIe once
+  (DESIGN.md §6).  A source that hands out pinned host rows (a pinned torch
+  tensor, a pinned ring) is copied straight from its pages; any other source
+  is read into two pinned staging buffers by a pool of host threads;
 * several GPUs in one process (``devices=[...]``): vertex-row slabs per GPU
   like split_blocks, histograms summed after the join.
 
@@ -25,6 +27,8 @@ for bit: integer sums commute.
 
 from __future__ import annotations
 
+import concurrent.futures as cf
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -84,6 +88,26 @@ def stream_hist(src, ndim, device, rows, chunk_bytes=DEFAULT_CHUNK_BYTES, hist=N
         return _stream_hist(src, ndim, device, rows, chunk_bytes, hist, kind)
 
 
+def _staging_threads():
+    return max(1, min(16, os.cpu_count() or 1))
+
+
+def _read_parallel(src, r0, r1, out, row_elems, pool):
+    """src.read_rows over [r0, r1) into ``out`` (numpy view of a pinned
+    buffer), split into row blocks read by the pool's threads: numpy copies
+    and file preads release the GIL, so a multi-core host fills the pinned
+    staging buffer at memory (or page-cache) speed instead of one core's."""
+    n = r1 - r0
+    parts = min(n, pool._max_workers)
+    if parts <= 1 or not getattr(src, "parallel_reads", False):
+        src.read_rows(r0, r1, out[: n * row_elems])
+        return
+    blocks = split_blocks(n, parts)
+    futs = [pool.submit(src.read_rows, r0 + lo, r0 + hi, out[lo * row_elems:hi * row_elems]) for lo, hi in blocks]
+    for f in futs:
+        f.result()
+
+
 def _stream_hist(src, ndim, device, rows, chunk_bytes, hist, kind):
     t = engine.torch()
     H = src.height
@@ -96,39 +120,64 @@ def _stream_hist(src, ndim, device, rows, chunk_bytes, hist, kind):
     vpc = max(1, cap - LOW_HALO)  # vertex rows per chunk (LOW_HALO halo rows re-sent)
     if hist is None:
         hist = kind.new(ndim, M, device)
-    host = getattr(src, "pinned_rows", None)  # a pinned torch tensor (rows, ...) or None
-    if host is None:
+    # a source that can hand out its rows as pinned host memory is copied
+    # straight from those pages (a pinned torch tensor, a pinned ring of
+    # planes); any other source is read into two pinned staging buffers
+    window = getattr(src, "pinned_window", None)
+    pool = None
+    if window is None:
         staging = [t.empty(cap * row_elems, dtype=tdt, pin_memory=True) for _ in range(2)]
         src.note_resident(2 * cap * row_elems * itemsize)
+        pool = cf.ThreadPoolExecutor(_staging_threads())
     dbuf = [t.empty(cap * row_elems, dtype=tdt, device=device) for _ in range(2)]
     compute = t.cuda.current_stream(device)
     copy = t.cuda.Stream(device)
-    copied = [t.cuda.Event() for _ in range(2)]
+    copied = [None, None]
     done = [None, None]
     v0, v1 = rows
-    for c, a in enumerate(range(v0, v1, vpc)):
-        b = min(a + vpc, v1)
-        s = c & 1
-        r0, r1 = held_rows(a, b, H)
-        n = (r1 - r0) * row_elems
-        if host is None:
-            if done[s] is not None:
-                done[s].synchronize()  # staging[s] free again
-            src.read_rows(r0, r1, staging[s].numpy()[:n])
-            chunk = staging[s][:n]
-        else:
-            chunk = host[r0 - src.pinned_first:r1 - src.pinned_first].reshape(-1)
-        with t.cuda.stream(copy):
-            if done[s] is not None:
-                copy.wait_event(done[s])  # dbuf[s] consumed by the previous kernel
-            dbuf[s][:n].copy_(chunk, non_blocking=True)
-            copied[s].record(copy)
-        compute.wait_event(copied[s])
-        view = dbuf[s][:n].view((r1 - r0,) + tuple(src.shape[1:]))
-        kind.launch(ndim, view, src.shape, M, src.quant, (a, b), first=r0, hist=hist)
-        ev = t.cuda.Event()
-        ev.record(compute)
-        done[s] = ev
+    prev = None  # (buffer, r0, r1) of the previous chunk
+    try:
+        for c, a in enumerate(range(v0, v1, vpc)):
+            b = min(a + vpc, v1)
+            s = c & 1
+            r0, r1 = held_rows(a, b, H)
+            # halo carry: the rows this chunk shares with the previous one
+            # (its last LOW_HALO rows) are copied device-to-device instead of
+            # crossing PCIe again; only rows [h0, r1) come from the host
+            carry = 0
+            if prev is not None and prev[1] <= r0 < prev[2]:
+                carry = prev[2] - r0
+            h0 = r0 + carry
+            n = (r1 - h0) * row_elems
+            if window is None and n:
+                if copied[s] is not None:
+                    copied[s].synchronize()  # staging[s] uploaded: free again
+                _read_parallel(src, h0, r1, staging[s].numpy(), row_elems, pool)
+                chunk = staging[s][:n]
+            elif n:
+                chunk = window(h0, r1).reshape(-1)
+            with t.cuda.stream(copy):
+                if done[s] is not None:
+                    copy.wait_event(done[s])  # dbuf[s] consumed by the previous kernel
+                if carry:  # after the previous chunk's upload (same stream)
+                    pb, p0, p1 = prev
+                    dbuf[s][:carry * row_elems].copy_(dbuf[pb][(r0 - p0) * row_elems:(p1 - p0) * row_elems],
+                                                      non_blocking=True)
+                if n:
+                    dbuf[s][carry * row_elems:carry * row_elems + n].copy_(chunk, non_blocking=True)
+                ev = t.cuda.Event()
+                ev.record(copy)
+                copied[s] = ev
+            compute.wait_event(copied[s])
+            view = dbuf[s][:(r1 - r0) * row_elems].view((r1 - r0,) + tuple(src.shape[1:]))
+            kind.launch(ndim, view, src.shape, M, src.quant, (a, b), first=r0, hist=hist)
+            ev = t.cuda.Event()
+            ev.record(compute)
+            done[s] = ev
+            prev = (s, r0, r1)
+    finally:
+        if pool is not None:
+            pool.shutdown(wait=True)
     return hist
 
 

@@ -166,3 +166,43 @@ def _global_extrema(shape, sigma, seed, device, chunk=256):
             del s
         _EXTREMA[key] = (lo, hi)
     return _EXTREMA[key]
+
+
+class PeriodicPlanes:
+    """Streaming source for fields larger than host memory (C5s: 4096^3 f32,
+    256 GiB): a (H, W, D) float32 field whose planes repeat with period P,
+    plane p = base[p % P], served from a PINNED ring holding the P base planes
+    twice, so any window of <= P planes is one contiguous pinned slice the
+    streaming engine DMAs from (``pinned_window``).  With a base generated
+    periodic along i (``grf_slab`` wraps), the tiled field is a smooth GRF of
+    the full size.  Bench / test helper, not part of the reference API."""
+
+    mode = "file-backed"
+    ndim = 3
+    parallel_reads = True
+
+    def __init__(self, ring, height, max_level, value_range):
+        from .quant import QuantSpec
+
+        P2, W, D = ring.shape
+        if P2 % 2 or not ring.is_pinned():
+            raise ValueError("ring must be a pinned (2P, W, D) tensor")
+        self.ring, self.P = ring, P2 // 2
+        self.height, self.width, self.depth = int(height), W, D
+        self.shape = (self.height, W, D)
+        self.dtype = np.dtype(np.float32)
+        self.max_level = int(max_level)
+        self.quant = QuantSpec.for_range(value_range[0], value_range[1], self.max_level)
+        self.peak_field_bytes = ring.numel() * ring.element_size()
+
+    def note_resident(self, nbytes):
+        self.peak_field_bytes = max(self.peak_field_bytes, nbytes)
+
+    def pinned_window(self, r0, r1):
+        if r1 - r0 > self.P:
+            raise ValueError(f"window of {r1 - r0} planes exceeds the ring period {self.P}")
+        s = r0 % self.P
+        return self.ring[s:s + (r1 - r0)]
+
+    def read_rows(self, r0, r1, out):
+        out.reshape(r1 - r0, -1)[:] = self.pinned_window(r0, r1).numpy().reshape(r1 - r0, -1)
