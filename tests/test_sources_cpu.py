@@ -71,3 +71,50 @@ def test_array_source_range_checks_identity_levels(tmp_path):
     with pytest.raises(ValueError):
         src.read_rows(0, 2, out)
     ft.ArraySource(np.full((3, 3), 2.5, np.float32), 7, value_range=(0.0, 8.0))  # samples: no check
+
+
+BMP_DIR = __import__("pathlib").Path(__file__).resolve().parent / "golden" / "bmp"
+
+
+@pytest.mark.parametrize("name", ["odd_7x5", "w8_8x3", "one_1x1"])
+def test_bmp_matches_reference_writer_bytes(tmp_path, name):
+    """write_bmp produces the reference writer's bytes (tests/golden/gen_bmp_golden.py)
+    and read_bmp / BmpSource read them back top row first."""
+    lv = np.load(BMP_DIR / f"{name}.npy")
+    out = tmp_path / "x.bmp"
+    ft.write_bmp(out, ft.Field2D(lv, 255))
+    assert out.read_bytes() == (BMP_DIR / f"{name}.bmp").read_bytes()
+    assert np.array_equal(ft.read_bmp(BMP_DIR / f"{name}.bmp").values, lv)
+    with ft.open_bmp_lowmem(BMP_DIR / f"{name}.bmp") as src:
+        assert (src.height, src.width) == lv.shape
+        assert src.sample_at(lv.shape[0] - 1, 0) == lv[-1, 0]
+        assert np.array_equal(src.read_row(0), lv[0].astype(np.uint8))
+        got = np.empty(lv.shape, np.uint8)
+        src.read_rows(0, lv.shape[0], got)
+        assert np.array_equal(got, lv)
+
+
+def test_bmp_top_down_and_errors(tmp_path):
+    raw = bytearray((BMP_DIR / "odd_7x5.bmp").read_bytes())
+    lv = np.load(BMP_DIR / "odd_7x5.npy")
+    # negative stored height: rows stored top-down
+    h = int.from_bytes(raw[22:26], "little", signed=True)
+    off = int.from_bytes(raw[10:14], "little")
+    stride = 8
+    rows = [bytes(raw[off + r * stride: off + (r + 1) * stride]) for r in range(h)]
+    td = raw[:off] + b"".join(rows[::-1])
+    td[22:26] = (-h).to_bytes(4, "little", signed=True)
+    p = tmp_path / "td.bmp"
+    p.write_bytes(bytes(td))
+    assert np.array_equal(ft.read_bmp(p).values, lv)
+    cases = {"bad magic": b"XM" + bytes(raw[2:]), "truncated BMP file header": bytes(raw[:10]),
+             "truncated BMP info header": bytes(raw[:30]), "truncated BMP pixel data": bytes(raw[:-3])}
+    for msg, data in cases.items():
+        p.write_bytes(data)
+        with pytest.raises(ValueError, match=msg):
+            ft.read_bmp(p)
+    bad = bytearray(raw)
+    bad[28:30] = (24).to_bytes(2, "little")
+    p.write_bytes(bytes(bad))
+    with pytest.raises(ValueError, match="only 8-bit BMP"):
+        ft.read_bmp(p)
