@@ -176,6 +176,51 @@ int ft_tables(int32_t ndim, int32_t *step, int32_t *src, int32_t *dst);
 int ft_quantize(const void *x, int32_t dtype, int64_t n, const ft_quant *q, int32_t M,
                 int32_t *out, void *stream);
 
+/* ------------------------------------------------------------ runtime */
+
+#define FT_KIND_MAP 0   /* transition-class histograms (ft_hist2d / ft_hist3d layout) */
+#define FT_KIND_FUSED 1 /* fused curve rows: 3D ft_lines3d [3][M+2], 2D ft_lines2d [4][M+2] (rows 0..2) */
+
+/* Out-of-core chunk streaming (the reference's low-memory mode,
+ * _stream_rows_2d / _stream_slabs_3d, contrib2d.py:235-251,
+ * contrib3d.py:392-414).  begin: a field of H rows/planes (W [x D] elements
+ * each, `dtype`, decoded by `q`; q->thresholds must stay valid until end)
+ * whose histogram `hist` (device, zeroed, layout of `kind`) is accumulated on
+ * `stream`; two device buffers of `chunk_rows` rows (>= 3).  push: the next
+ * `nrows` consecutive rows from host (pinned or pageable) or device memory,
+ * any batch size; copies run on an internal stream into the buffer being
+ * filled, the 2 rows a full buffer shares with the next are carried
+ * device-to-device, and the kernel for every vertex row whose planes have
+ * arrived runs on `stream` while the next buffer fills.  end: after all H
+ * rows were pushed, books the last vertex rows, waits for `stream` and frees
+ * the state (also on error).  Replaces the Python-level window loops with
+ * one native engine (gather.stream_hist is its Python twin). */
+typedef struct ft_stream ft_stream;
+int ft_stream_begin(int32_t ndim, int64_t H, int64_t W, int64_t D, int32_t dtype, const ft_quant *q, int32_t M,
+                    int32_t kind, int64_t chunk_rows, uint64_t *hist, void *stream, ft_stream **out);
+int ft_stream_push(ft_stream *s, const void *rows, int64_t nrows);
+int ft_stream_end(ft_stream *s);
+
+/* One slab of a field spread over several GPUs of this process: planes
+ * `win` resident on `device` (with `quant`'s thresholds on that device) and
+ * the vertex rows [v0, v1) it books into `hist` (device memory on `device`,
+ * zeroed, layout of `kind`). */
+typedef struct ft_slab {
+    int32_t device;
+    ft_window win;
+    int64_t v0, v1;
+    ft_quant quant;
+    uint64_t *hist;
+} ft_slab;
+
+/* The reference's worker split (_parallel.py:8-33) across GPUs: every slab's
+ * histogram on its own device, then ONE all-reduce so that every slab's
+ * `hist` holds the whole-field histogram -- ncclAllReduce (sum, uint64) when
+ * all devices are distinct and NCCL is loadable (*used_nccl = 1), else a
+ * peer-copy reduction.  Synchronous: returns when every hist is final. */
+int ft_multi_gather3d(const ft_slab *slabs, int32_t nslab, int64_t H, int64_t W, int64_t D, int32_t M, int32_t kind,
+                      int32_t *used_nccl);
+
 /* Verification hook (tests only, not a reference interface): run one of the
  * three device quantizers the fused kernels inline -- path 0 to_level (map /
  * wide kernels, ft_quantize), 1 to_level4 (march / lattice kernels, incl. the

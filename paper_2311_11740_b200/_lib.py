@@ -17,7 +17,9 @@ FT_Q_IDENTITY, FT_Q_TABLE, FT_Q_TABLE_ROBUST, FT_Q_POW2 = 0, 1, 2, 3
 FT_ERR_ARG, FT_ERR_CLASSIFY, FT_ERR_INTERNAL, FT_ERR_CUDA_BASE = 1, 2, 3, 1000
 
 EXPORTS = ("ft_hist2d", "ft_hist3d", "ft_lattice2d", "ft_lattice3d", "ft_lines3d", "ft_lines3d_ok", "ft_lines2d", "ft_lines2d_ok", "ft_finalize", "ft_curves", "ft_class_weights", "ft_tables",
-           "ft_quantize", "ft_quantize_probe", "ft_minmax", "ft_key_to_double", "ft_key64_to_double", "ft_version")
+           "ft_quantize", "ft_quantize_probe", "ft_minmax", "ft_key_to_double", "ft_key64_to_double", "ft_version",
+           "ft_stream_begin", "ft_stream_push", "ft_stream_end", "ft_multi_gather3d")
+FT_KIND_MAP, FT_KIND_FUSED = 0, 1
 
 
 class ft_quant(ctypes.Structure):
@@ -28,6 +30,11 @@ class ft_quant(ctypes.Structure):
 class ft_window(ctypes.Structure):
     _fields_ = [("data", ctypes.c_void_p), ("dtype", ctypes.c_int32), ("first", ctypes.c_int64),
                 ("count", ctypes.c_int64), ("batch", ctypes.c_int64), ("batch_stride", ctypes.c_int64)]
+
+
+class ft_slab(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int32), ("win", ft_window), ("v0", ctypes.c_int64), ("v1", ctypes.c_int64),
+                ("quant", ft_quant), ("hist", ctypes.c_void_p)]
 
 
 _lock = threading.Lock()
@@ -73,6 +80,10 @@ def load(build_if_missing=True):
         L.ft_key64_to_double.argtypes = [ctypes.c_uint64]
         L.ft_key64_to_double.restype = ctypes.c_double
         L.ft_version.restype = ctypes.c_char_p
+        L.ft_stream_begin.argtypes = [i32, i64, i64, i64, i32, P(ft_quant), i32, i32, i64, vp, vp, P(vp)]
+        L.ft_stream_push.argtypes = [vp, vp, i64]
+        L.ft_stream_end.argtypes = [vp]
+        L.ft_multi_gather3d.argtypes = [P(ft_slab), i32, i64, i64, i64, i32, i32, P(i32)]
         for name in EXPORTS:
             if name not in ("ft_key_to_double", "ft_key64_to_double", "ft_version"):
                 getattr(L, name).restype = ctypes.c_int

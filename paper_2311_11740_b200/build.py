@@ -73,7 +73,7 @@ def build(force=False, verbose=False, ptxas_info=False):
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(compile_one, _sources()))
     tmp = LIB.with_suffix(f".{os.getpid()}.tmp")
-    cmd = [cc, *ARCH, "-shared", "-o", str(tmp), *map(str, objs)]
+    cmd = [cc, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc link failed:\n{res.stderr}")

@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(HM_NTH, 2) hist2d_march(const typename Elem<DT
     uint32_t* h = reinterpret_cast<uint32_t*>(smem_raw);  // 6 class rows + the dummy row
     float* tt = reinterpret_cast<float*>(h + 7 * M2);
     for (int i = threadIdx.x; i < 7 * M2; i += blockDim.x) h[i] = 0;
-    if (QM != FT_Q_IDENTITY)
+    if (QM != FT_Q_IDENTITY && QM != FT_Q_POW2)
         for (int i = threadIdx.x; i < M2; i += blockDim.x) tt[i] = q.tt[i];
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -275,7 +275,8 @@ static int launch2(const ft_window* win, int64_t H, int64_t W, int64_t v0, int64
     }
     const int64_t n = g.batch * (v1 - v0) * (W + 1);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), (int64_t)nsm * 8));
-    hist2d_wide<DT, QM><<<grid, 256, 0, st>>>(buf, g, q, out);
+    constexpr int QW = QM == FT_Q_POW2 ? FT_Q_TABLE : QM;  // the table ships with FT_Q_POW2 too
+    hist2d_wide<DT, QW><<<grid, 256, 0, st>>>(buf, g, q, out);
     FT_CUDA_TRY(cudaGetLastError());
     return FT_OK;
 }
@@ -294,7 +295,7 @@ extern "C" int ft_hist2d(const ft_window* win, int64_t H, int64_t W, int64_t v0,
     if (need_lo <= need_hi && (win->data == nullptr || need_lo < win->first || need_hi >= win->first + win->count))
         return FT_ERR_ARG;
     if (M > (1 << 29) - 2) return FT_ERR_ARG;  // keys level*4 + slot in 32 bits
-    const int qm = effective_qmode(q);
+    const int qm = effective_qmode(q, true);  // FT_Q_POW2: table-free march quantizer
     if (qm != FT_Q_IDENTITY && !q->thresholds) return FT_ERR_ARG;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     switch (win->dtype) {
@@ -303,14 +304,16 @@ extern "C" int ft_hist2d(const ft_window* win, int64_t H, int64_t W, int64_t v0,
         return launch2<FT_I32, FT_Q_IDENTITY>(win, H, W, v0, v1, q, M, hist, st);
     case FT_U8:
         if (qm == FT_Q_IDENTITY) return launch2<FT_U8, FT_Q_IDENTITY>(win, H, W, v0, v1, q, M, hist, st);
-        if (qm == FT_Q_TABLE) return launch2<FT_U8, FT_Q_TABLE>(win, H, W, v0, v1, q, M, hist, st);
+        if (qm == FT_Q_TABLE || qm == FT_Q_POW2) return launch2<FT_U8, FT_Q_TABLE>(win, H, W, v0, v1, q, M, hist, st);
         return launch2<FT_U8, FT_Q_TABLE_ROBUST>(win, H, W, v0, v1, q, M, hist, st);
     case FT_U16:
         if (qm == FT_Q_IDENTITY) return launch2<FT_U16, FT_Q_IDENTITY>(win, H, W, v0, v1, q, M, hist, st);
+        if (qm == FT_Q_POW2) return launch2<FT_U16, FT_Q_POW2>(win, H, W, v0, v1, q, M, hist, st);
         if (qm == FT_Q_TABLE) return launch2<FT_U16, FT_Q_TABLE>(win, H, W, v0, v1, q, M, hist, st);
         return launch2<FT_U16, FT_Q_TABLE_ROBUST>(win, H, W, v0, v1, q, M, hist, st);
     case FT_F32:
         if (qm == FT_Q_IDENTITY) return FT_ERR_ARG;
+        if (qm == FT_Q_POW2) return launch2<FT_F32, FT_Q_POW2>(win, H, W, v0, v1, q, M, hist, st);
         if (qm == FT_Q_TABLE) return launch2<FT_F32, FT_Q_TABLE>(win, H, W, v0, v1, q, M, hist, st);
         return launch2<FT_F32, FT_Q_TABLE_ROBUST>(win, H, W, v0, v1, q, M, hist, st);
     }

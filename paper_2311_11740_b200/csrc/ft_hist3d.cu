@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(HM3_NTH, 1) hist3d_march(const typename Elem<D
     uint32_t* ta = h + 40 * M2;
     uint32_t* tb = ta + NTAB;
     float* tt = reinterpret_cast<float*>(tb + NTAB);
-    init_shared3(h, ta, tb, tt, rt, q, M2, QM != FT_Q_IDENTITY);
+    init_shared3(h, ta, tb, tt, rt, q, M2, QM != FT_Q_IDENTITY && QM != FT_Q_POW2);
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int TJ = (HM3_NTH / 32) * HMR;
@@ -417,7 +417,8 @@ static int launch3(const ft_window* win, int64_t H, int64_t W, int64_t D, int64_
     }
     const int64_t n = (v1 - v0) * (W + 1) * (D + 1);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), (int64_t)nsm * 8));
-    hist3d_wide<DT, QM><<<grid, 256, 0, st>>>(buf, g, q, rt, out);
+    constexpr int QW = QM == FT_Q_POW2 ? FT_Q_TABLE : QM;  // the table ships with FT_Q_POW2 too
+    hist3d_wide<DT, QW><<<grid, 256, 0, st>>>(buf, g, q, rt, out);
     FT_CUDA_TRY(cudaGetLastError());
     return FT_OK;
 }
@@ -437,7 +438,8 @@ extern "C" int ft_hist3d(const ft_window* win, int64_t H, int64_t W, int64_t D, 
     if (need_lo <= need_hi && (win->data == nullptr || need_lo < win->first || need_hi >= win->first + win->count))
         return FT_ERR_ARG;
     if (M > (1 << 28) - 2) return FT_ERR_ARG;  // keys level*8 + slot in 32 bits
-    const int qm = effective_qmode(q);
+    // FT_Q_POW2 (lo = 0, hi = 2^p): the march quantizes without the table
+    const int qm = effective_qmode(q, true);
     if (qm != FT_Q_IDENTITY && (!q->thresholds || win->dtype == FT_I32)) return FT_ERR_ARG;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     switch (win->dtype) {
@@ -446,14 +448,16 @@ extern "C" int ft_hist3d(const ft_window* win, int64_t H, int64_t W, int64_t D, 
         return launch3<FT_I32, FT_Q_IDENTITY>(win, H, W, D, v0, v1, q, M, hist, st);
     case FT_U8:
         if (qm == FT_Q_IDENTITY) return launch3<FT_U8, FT_Q_IDENTITY>(win, H, W, D, v0, v1, q, M, hist, st);
-        if (qm == FT_Q_TABLE) return launch3<FT_U8, FT_Q_TABLE>(win, H, W, D, v0, v1, q, M, hist, st);
+        if (qm == FT_Q_TABLE || qm == FT_Q_POW2) return launch3<FT_U8, FT_Q_TABLE>(win, H, W, D, v0, v1, q, M, hist, st);
         return launch3<FT_U8, FT_Q_TABLE_ROBUST>(win, H, W, D, v0, v1, q, M, hist, st);
     case FT_U16:
         if (qm == FT_Q_IDENTITY) return launch3<FT_U16, FT_Q_IDENTITY>(win, H, W, D, v0, v1, q, M, hist, st);
+        if (qm == FT_Q_POW2) return launch3<FT_U16, FT_Q_POW2>(win, H, W, D, v0, v1, q, M, hist, st);
         if (qm == FT_Q_TABLE) return launch3<FT_U16, FT_Q_TABLE>(win, H, W, D, v0, v1, q, M, hist, st);
         return launch3<FT_U16, FT_Q_TABLE_ROBUST>(win, H, W, D, v0, v1, q, M, hist, st);
     case FT_F32:
         if (qm == FT_Q_IDENTITY) return FT_ERR_ARG;
+        if (qm == FT_Q_POW2) return launch3<FT_F32, FT_Q_POW2>(win, H, W, D, v0, v1, q, M, hist, st);
         if (qm == FT_Q_TABLE) return launch3<FT_F32, FT_Q_TABLE>(win, H, W, D, v0, v1, q, M, hist, st);
         return launch3<FT_F32, FT_Q_TABLE_ROBUST>(win, H, W, D, v0, v1, q, M, hist, st);
     }

@@ -342,3 +342,70 @@ def as_uint64(t):
 
 __all__ = ["launch_hist", "finalize", "curves_from_maps", "quantize_device", "minmax_device", "to_device",
            "default_device", "new_hist", "as_uint64", "class_weights", "QuantSpec"]
+
+
+def stream_native(rows, shape, M, quant, kind="map", chunk_rows=64, push_rows=None, device=None, hist=None):
+    """Histogram of a field pushed row block by row block through the native
+    streaming engine (ft_stream_begin / push / end: the C-ABI twin of
+    gather.stream_hist for non-Python callers).  ``rows``: the whole field
+    as a host numpy array (pageable), a pinned / CPU torch tensor or a CUDA
+    tensor -- it is only READ, ``push_rows`` rows per ft_stream_push."""
+    t = torch()
+    L = _lib.load()
+    dev = default_device(device)
+    ndim = len(shape)
+    H, W = shape[0], shape[1]
+    D = shape[2] if ndim == 3 else 1
+    k = _lib.FT_KIND_MAP if kind == "map" else _lib.FT_KIND_FUSED
+    if hist is None:
+        hist = new_hist(ndim, M, dev) if kind == "map" else (new_lines_hist(M, dev) if ndim == 3
+                                                            else new_lattice_hist(2, M, dev))
+    if isinstance(rows, np.ndarray):
+        a = np.ascontiguousarray(rows)
+        ptr, code, row_bytes = a.ctypes.data, dtype_code(t.from_numpy(a[:1].copy())), a[0].nbytes
+    else:
+        a = rows.contiguous()
+        ptr, code, row_bytes = a.data_ptr(), dtype_code(a), a[0].numel() * a.element_size()
+    push_rows = push_rows or chunk_rows
+    with on_device(dev):
+        qs, keep = device_struct(quant, dev)
+        h = ctypes.c_void_p()
+        _lib.check(L.ft_stream_begin(ndim, H, W, D, code, ctypes.byref(qs), M, k, chunk_rows,
+                                     ctypes.c_void_p(hist.data_ptr()), _stream_ptr(dev), ctypes.byref(h)),
+                   "ft_stream_begin")
+        try:
+            for r in range(0, H, push_rows):
+                n = min(push_rows, H - r)
+                _lib.check(L.ft_stream_push(h, ctypes.c_void_p(ptr + r * row_bytes), n), "ft_stream_push")
+        finally:
+            rc = L.ft_stream_end(h)
+        _lib.check(rc, "ft_stream_end")
+    del keep, a
+    return hist
+
+
+def multi_gather_native(parts, shape, M, quant, kind="map"):
+    """ft_multi_gather3d over ``parts`` = [(CUDA tensor of planes [r0, r1),
+    r0, (v0, v1))] (one per slab, any devices); returns (per-slab histogram
+    tensors, each holding the whole-field sum, used_nccl)."""
+    L = _lib.load()
+    H, W, D = shape
+    k = _lib.FT_KIND_MAP if kind == "map" else _lib.FT_KIND_FUSED
+    slabs = (_lib.ft_slab * len(parts))()
+    keep, hists = [], []
+    for s, (x, r0, (v0, v1)) in zip(slabs, parts):
+        with on_device(x.device):
+            qs, kt = device_struct(quant, x.device)
+            h = new_hist(3, M, x.device) if kind == "map" else new_lines_hist(M, x.device)
+        keep += [kt, x]
+        hists.append(h)
+        s.device = x.device.index
+        s.win = _lib.ft_window(ctypes.c_void_p(x.data_ptr()), dtype_code(x), int(r0), int(x.shape[0]), 1, 0)
+        s.v0, s.v1 = int(v0), int(v1)
+        s.quant = qs
+        s.hist = ctypes.c_void_p(h.data_ptr())
+    torch().cuda.synchronize()  # histograms zeroed before the library's own streams use them
+    used = ctypes.c_int32(0)
+    _lib.check(L.ft_multi_gather3d(slabs, len(parts), H, W, D, M, k, ctypes.byref(used)), "ft_multi_gather3d")
+    del keep
+    return hists, bool(used.value)

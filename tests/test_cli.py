@@ -28,3 +28,22 @@ def test_usage_errors_exit_1(argv, tmp_path, monkeypatch, capsys):
 def test_parser_defaults():
     a = build_parser().parse_args(["bench", "--generate", "8x8"])
     assert (a.repeats, a.workers, a.max_level, a.path, a.dist) == (5, 1, 255, "map", "uniform")
+
+
+def test_internal_consistency_failure_exits_2(tmp_path, monkeypatch, capsys):
+    """A ClassificationError from the gather (reference contrib3d.py:425-426)
+    is reported as an internal consistency failure with exit code 2
+    (reference cli.py:271-273, pkg/tests/test_cli.py:139-150)."""
+    import numpy as np
+
+    import paper_2311_11740_b200 as ft
+    from paper_2311_11740_b200 import cli
+
+    def boom(source, workers, **kw):
+        raise ft.ClassificationError("q-table miss")
+
+    monkeypatch.setattr(cli, "gather_2d_parallel", boom)
+    p = tmp_path / "x.bmp"
+    ft.write_bmp(p, ft.Field2D(np.zeros((1, 1), np.int32), 255))
+    assert main(["curve", "--input", str(p)]) == 2
+    assert "internal consistency" in capsys.readouterr().err
