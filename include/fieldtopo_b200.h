@@ -221,6 +221,12 @@ typedef struct ft_slab {
 int ft_multi_gather3d(const ft_slab *slabs, int32_t nslab, int64_t H, int64_t W, int64_t D, int32_t M, int32_t kind,
                       int32_t *used_nccl);
 
+/* 8-bit BMP pixel data as stored in the file (H rows of row_stride bytes,
+ * bottom-up when bottom_up != 0) -> compact top-first H x W uint8 levels on
+ * the device (reference read_bmp, sources.py:154-164: row flip + unpadding). */
+int ft_bmp_decode(const uint8_t *raw, int64_t H, int64_t W, int64_t row_stride, int32_t bottom_up, uint8_t *out,
+                  void *stream);
+
 /* Verification hook (tests only, not a reference interface): run one of the
  * three device quantizers the fused kernels inline -- path 0 to_level (map /
  * wide kernels, ft_quantize), 1 to_level4 (march / lattice kernels, incl. the

@@ -299,3 +299,29 @@ extern "C" double ft_key_to_double(int32_t dtype, uint32_t key)
     default: return (double)key;
     }
 }
+
+// ------------------------------------------------------ BMP pixel decode
+// 8-bit BMP pixel rows as stored (padded to 4 bytes, bottom-up when the
+// header height is positive) -> compact top-first rows (reference read_bmp,
+// sources.py:154-164, on the device).  One thread per output pixel quad.
+__global__ void bmp_decode_kernel(const uint8_t* __restrict__ raw, int64_t H, int64_t W, int64_t stride,
+                                  int bottom_up, uint8_t* __restrict__ out)
+{
+    const int64_t n = H * W;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / W, c = i - r * W;
+        const int64_t src_row = bottom_up ? H - 1 - r : r;
+        out[i] = raw[src_row * stride + c];
+    }
+}
+
+extern "C" int ft_bmp_decode(const uint8_t* raw, int64_t H, int64_t W, int64_t row_stride, int32_t bottom_up,
+                             uint8_t* out, void* stream)
+{
+    if (!raw || !out || H < 1 || W < 1 || row_stride < W) return FT_ERR_ARG;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(H * W, 256), 16 * nsm()));
+    bmp_decode_kernel<<<grid, 256, 0, st>>>(raw, H, W, row_stride, bottom_up ? 1 : 0, out);
+    FT_CUDA_TRY(cudaGetLastError());
+    return FT_OK;
+}

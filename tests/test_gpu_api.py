@@ -67,3 +67,23 @@ def test_calls_follow_the_tensor_device(ft, orc):
     if torch.cuda.device_count() > 1:  # a resident field is not moved to another GPU
         with pytest.raises(ValueError):
             ft.gather_3d_serial(src, device="cuda:1")
+
+
+def test_read_bmp_device_decode(ft, orc, tmp_path):
+    """BMP pixel decode (row flip + unpadding) on the device equals the host
+    read_bmp (reference sources.py:154-164) on the reference writer's
+    fixtures and on random sizes, and gathers like the host field."""
+    from pathlib import Path
+    bdir = Path(__file__).resolve().parent / "golden" / "bmp"
+    for name in ("odd_7x5", "w8_8x3", "one_1x1"):
+        src = ft.read_bmp_device(bdir / f"{name}.bmp")
+        assert np.array_equal(src.tensor.cpu().numpy(), np.load(bdir / f"{name}.npy"))
+    for shape in ((33, 61), (64, 64), (3, 130)):
+        lv = np.random.default_rng(shape[1]).integers(0, 256, size=shape).astype(np.int32)
+        p = tmp_path / "r.bmp"
+        ft.write_bmp(p, ft.Field2D(lv, 255))
+        src = ft.read_bmp_device(p)
+        assert np.array_equal(src.tensor.cpu().numpy(), lv)
+        q_in, q_out = orc.gather2d(lv, 255)
+        m = ft.gather_2d_serial(src)
+        assert np.array_equal(m.q_in, q_in) and np.array_equal(m.q_out, q_out)
