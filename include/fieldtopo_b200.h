@@ -221,6 +221,16 @@ typedef struct ft_slab {
 int ft_multi_gather3d(const ft_slab *slabs, int32_t nslab, int64_t H, int64_t W, int64_t D, int32_t M, int32_t kind,
                       int32_t *used_nccl);
 
+/* Classification status of the 3D map kernels since the last call (waits for
+ * `stream`): FT_ERR_CLASSIFY when a vertex neighbourhood fell outside the
+ * configuration table -- the reference's ValueError (contrib3d.py:304-305,
+ * 330) / ClassificationError (contrib3d.py:425-426) -- else FT_OK.  The
+ * tables are total over the 8! slot orders, so only a corrupted table can
+ * trip it; ft_debug_trap_tables(1) (tests only) installs such a table on the
+ * current device and ft_debug_trap_tables(0) restores the real one. */
+int ft_classify_status(void *stream);
+int ft_debug_trap_tables(int32_t on);
+
 /* 8-bit BMP pixel data as stored in the file (H rows of row_stride bytes,
  * bottom-up when bottom_up != 0) -> compact top-first H x W uint8 levels on
  * the device (reference read_bmp, sources.py:154-164: row flip + unpadding). */

@@ -18,7 +18,8 @@ FT_ERR_ARG, FT_ERR_CLASSIFY, FT_ERR_INTERNAL, FT_ERR_CUDA_BASE = 1, 2, 3, 1000
 
 EXPORTS = ("ft_hist2d", "ft_hist3d", "ft_lattice2d", "ft_lattice3d", "ft_lines3d", "ft_lines3d_ok", "ft_lines2d", "ft_lines2d_ok", "ft_finalize", "ft_curves", "ft_class_weights", "ft_tables",
            "ft_quantize", "ft_quantize_probe", "ft_minmax", "ft_key_to_double", "ft_key64_to_double", "ft_version",
-           "ft_stream_begin", "ft_stream_push", "ft_stream_end", "ft_multi_gather3d", "ft_bmp_decode")
+           "ft_stream_begin", "ft_stream_push", "ft_stream_end", "ft_multi_gather3d", "ft_bmp_decode",
+           "ft_classify_status", "ft_debug_trap_tables")
 FT_KIND_MAP, FT_KIND_FUSED = 0, 1
 
 
@@ -83,6 +84,8 @@ def load(build_if_missing=True):
         L.ft_stream_begin.argtypes = [i32, i64, i64, i64, i32, P(ft_quant), i32, i32, i64, vp, vp, P(vp)]
         L.ft_stream_push.argtypes = [vp, vp, i64]
         L.ft_bmp_decode.argtypes = [vp, i64, i64, i64, i32, vp, vp]
+        L.ft_classify_status.argtypes = [vp]
+        L.ft_debug_trap_tables.argtypes = [i32]
         L.ft_stream_end.argtypes = [vp]
         L.ft_multi_gather3d.argtypes = [P(ft_slab), i32, i64, i64, i64, i32, i32, P(i32)]
         for name in EXPORTS:

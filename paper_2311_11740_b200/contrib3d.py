@@ -113,6 +113,7 @@ def accumulate_vertex_3d(nbhd, cmap):
 
 
 def _map_from_hist(src, hist):
+    engine.check_classification(hist.device)  # contrib3d.py:425-426
     q_in, q_out, _ = engine.finalize(3, src.max_level, hist, maps=True)
     return ContributionMap3D(src.width, src.height, src.depth, src.max_level, engine.as_uint64(q_in),
                              engine.as_uint64(q_out))

@@ -28,6 +28,14 @@
 namespace ft {
 
 constexpr int NTAB = 4096;            // rank-group table entries
+// Classification failures (the reference raises ValueError "3D neighborhood
+// outside the configuration table", contrib3d.py:304-305/330, re-raised as
+// ClassificationError, contrib3d.py:425-426): table entries of impossible
+// slot tuples name the TRAP class; its shared row is never flushed into the
+// histogram but sets ft_trap3, which ft_classify_status reports.
+constexpr uint32_t TRAP = 40;
+constexpr int NROW3 = 41;             // 40 transition classes + the trap row
+__device__ unsigned int ft_trap3 = 0;
 
 struct Geo3 {
     int64_t H, W, D, v0, v1, first;
@@ -60,7 +68,7 @@ __device__ __forceinline__ void init_shared3(uint32_t* h, uint32_t* ta, uint32_t
                                              const RankTables* __restrict__ rt, const QuantDev& q, int M2,
                                              bool table)
 {
-    for (int i = threadIdx.x; i < 40 * M2; i += blockDim.x) h[i] = 0;
+    for (int i = threadIdx.x; i < NROW3 * M2; i += blockDim.x) h[i] = 0;
     for (int i = threadIdx.x; i < NTAB; i += blockDim.x) {
         ta[i] = rt->a[i];
         tb[i] = rt->b[i];
@@ -69,12 +77,14 @@ __device__ __forceinline__ void init_shared3(uint32_t* h, uint32_t* ta, uint32_t
         for (int i = threadIdx.x; i < M2; i += blockDim.x) tt[i] = q.tt[i];
 }
 
-__device__ __forceinline__ void flush_hist(const uint32_t* h, unsigned long long* __restrict__ hist, int n)
+__device__ __forceinline__ void flush_hist(const uint32_t* h, unsigned long long* __restrict__ hist, int M2)
 {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    for (int i = threadIdx.x; i < 40 * M2; i += blockDim.x) {
         uint32_t v = h[i];
         if (v) atomicAdd(&hist[i], (unsigned long long)v);
     }
+    for (int i = threadIdx.x; i < M2; i += blockDim.x)
+        if (h[TRAP * M2 + i]) atomicOr(&ft_trap3, 1u);
 }
 
 // Two-vertex (packed 16-bit halves) compare-exchange networks: VIMNMX.U16x2.
@@ -258,7 +268,7 @@ __global__ void __launch_bounds__(HM3_NTH, 1) hist3d_march(const typename Elem<D
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int M2 = g.M + 2;
     uint32_t* h = reinterpret_cast<uint32_t*>(smem_raw);
-    uint32_t* ta = h + 40 * M2;
+    uint32_t* ta = h + NROW3 * M2;
     uint32_t* tb = ta + NTAB;
     float* tt = reinterpret_cast<float*>(tb + NTAB);
     init_shared3(h, ta, tb, tt, rt, q, M2, QM != FT_Q_IDENTITY && QM != FT_Q_POW2);
@@ -284,7 +294,7 @@ __global__ void __launch_bounds__(HM3_NTH, 1) hist3d_march(const typename Elem<D
             hm3_item<DT, QM, VEC, true>(buf, g, q, tt, h, ta, tb, ia, ia + len, j0, k0, lane);
     }
     __syncthreads();
-    flush_hist(h, hist, 40 * M2);
+    flush_hist(h, hist, M2);
 }
 
 // Any level count: one vertex per thread (k fastest: coalesced cell loads,
@@ -320,7 +330,12 @@ __global__ void __launch_bounds__(256) hist3d_wide(const typename Elem<DT>::T* _
         const uint32_t cls[8] = {0u, ea & 0xFFu, (ea >> 8) & 0xFFu, ea >> 16, eb & 0xFFu, (eb >> 8) & 0xFFu,
                                  eb >> 16, 39u};
 #pragma unroll
-        for (int r8 = 0; r8 < 8; ++r8) atomicAdd(&hist[cls[r8] * M2 + (a[r8] >> 3)], 1ull);
+        for (int r8 = 0; r8 < 8; ++r8) {
+            if (cls[r8] < TRAP)
+                atomicAdd(&hist[cls[r8] * M2 + (a[r8] >> 3)], 1ull);
+            else
+                atomicOr(&ft_trap3, 1u);
+        }
     }
 }
 
@@ -335,12 +350,14 @@ static RankTables make_rank_tables()
         bool distinct = true;
         for (int x = 0; x < 4; ++x)
             for (int y = x + 1; y < 4; ++y) distinct &= s[x] != s[y];
-        if (!distinct) continue;
+        rt.a[idx] = rt.b[idx] = TRAP * 0x010101u;
+        if (!distinct) continue;  // unreachable: a vertex's 8 slots are distinct
         // ranks 1..3: masks {s0}, {s0,s1}, {s0,s1,s2}
         int m = 1 << s[0];
         uint32_t ea = 0;
         for (int r = 1; r <= 3; ++r) {
-            ea |= (uint32_t)t.step[m * 8 + s[r]] << (8 * (r - 1));
+            const int c = t.step[m * 8 + s[r]];
+            ea |= (uint32_t)(c >= 0 ? c : (int)TRAP) << (8 * (r - 1));
             m |= 1 << s[r];
         }
         rt.a[idx] = ea;
@@ -349,7 +366,8 @@ static RankTables make_rank_tables()
         int mb = 0xFF & ~((1 << s[0]) | (1 << s[1]) | (1 << s[2]) | (1 << s[3]));
         uint32_t eb = 0;
         for (int r = 0; r < 3; ++r) {
-            eb |= (uint32_t)t.step[mb * 8 + s[r]] << (8 * r);
+            const int c = t.step[mb * 8 + s[r]];
+            eb |= (uint32_t)(c >= 0 ? c : (int)TRAP) << (8 * r);
             mb |= 1 << s[r];
         }
         rt.b[idx] = eb;
@@ -381,7 +399,7 @@ static const RankTables* device_rank_tables()
 }
 
 // shared bytes of hist3d_march: the 40 x (M+2) histogram, both rank tables, the threshold table
-static size_t march3_smem(int M) { return (size_t)(40 * (M + 2) + 2 * NTAB + (M + 2)) * 4; }
+static size_t march3_smem(int M) { return (size_t)(NROW3 * (M + 2) + 2 * NTAB + (M + 2)) * 4; }
 static bool march3_ok(int M) { return M + 1 <= 8190 && march3_smem(M) <= 227 * 1024; }
 
 template <int DT, int QM>
@@ -426,6 +444,32 @@ static int launch3(const ft_window* win, int64_t H, int64_t W, int64_t D, int64_
 }  // namespace ft
 
 using namespace ft;
+
+extern "C" int ft_classify_status(void* stream)
+{
+    FT_CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    unsigned int v = 0;
+    FT_CUDA_TRY(cudaMemcpyFromSymbol(&v, ft_trap3, sizeof(v)));
+    if (v) {
+        const unsigned int zero = 0;
+        FT_CUDA_TRY(cudaMemcpyToSymbol(ft_trap3, &zero, sizeof(zero)));
+    }
+    return v ? FT_ERR_CLASSIFY : FT_OK;
+}
+
+extern "C" int ft_debug_trap_tables(int32_t on)
+{
+    const RankTables* d = device_rank_tables();
+    if (!d) return FT_ERR_CUDA_BASE + (int)cudaErrorMemoryAllocation;
+    static const RankTables good = make_rank_tables();
+    static const RankTables bad = [] {
+        RankTables r = make_rank_tables();
+        for (int i = 0; i < NTAB; ++i) r.a[i] = r.b[i] = TRAP * 0x010101u;
+        return r;
+    }();
+    FT_CUDA_TRY(cudaMemcpy(const_cast<RankTables*>(d), on ? &bad : &good, sizeof(RankTables), cudaMemcpyHostToDevice));
+    return FT_OK;
+}
 
 extern "C" int ft_hist3d(const ft_window* win, int64_t H, int64_t W, int64_t D, int64_t v0, int64_t v1,
                          const ft_quant* q, int32_t M, uint64_t* hist, void* stream)

@@ -120,6 +120,8 @@ def gather_distributed(x, shape, max_level, value_range=None, group=None):
     M = int(max_level)
     quant = QuantSpec.for_range(*value_range, M) if value_range is not None else QuantSpec.identity()
     hist = all_reduce_hist(local_hist(ndim, x, shape, slab, M, quant), group)
+    if ndim == 3:
+        engine.check_classification(hist.device)
     q_in, q_out, _ = engine.finalize(ndim, M, hist, maps=True)
     qi, qo = engine.as_uint64(q_in), engine.as_uint64(q_out)
     if ndim == 2:

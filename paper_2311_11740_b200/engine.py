@@ -285,6 +285,14 @@ def finalize(ndim, M, hist, maps=True, tables=()):
     return q_in, q_out, num
 
 
+def check_classification(device):
+    """Raise ClassificationError if a 3D map kernel on ``device`` met a
+    neighbourhood outside the configuration table since the last check
+    (ft_classify_status; waits for the device's current stream)."""
+    with on_device(device):
+        _lib.check(_lib.load().ft_classify_status(_stream_ptr(device)), "ft_hist3d")
+
+
 def curves_from_maps(q_in, q_out, M, eighths_list, device):
     """descriptor_curve / counts_at_levels on device: weighted prefix scan of
     the rows (q_in; q_out) with weights (w; -w)."""

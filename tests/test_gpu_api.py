@@ -87,3 +87,24 @@ def test_read_bmp_device_decode(ft, orc, tmp_path):
         q_in, q_out = orc.gather2d(lv, 255)
         m = ft.gather_2d_serial(src)
         assert np.array_equal(m.q_in, q_in) and np.array_equal(m.q_out, q_out)
+
+
+def test_classification_trap_raises(ft, tmp_path, capsys):
+    """A neighbourhood outside the configuration table raises
+    ClassificationError (reference contrib3d.py:425-426) and the CLI exits
+    with 2 (cli.py:271-273).  The real tables are total, so a corrupted table
+    is installed for the test (ft_debug_trap_tables) and restored after."""
+    from paper_2311_11740_b200 import _lib
+    from paper_2311_11740_b200.cli import main
+    L = _lib.load()
+    f = ft.random_field((6, 5, 4), seed=1, max_level=15)
+    good = ft.gather_3d_serial(f)
+    _lib.check(L.ft_debug_trap_tables(1))
+    try:
+        with pytest.raises(ft.ClassificationError):
+            ft.gather_3d_serial(f)
+        assert main(["contrib-dump", "--generate", "6x5x4", "--seed", "1", "--max-level", "15"]) == 2
+        assert "internal consistency" in capsys.readouterr().err
+    finally:
+        _lib.check(L.ft_debug_trap_tables(0))
+    assert ft.gather_3d_serial(f) == good
