@@ -42,7 +42,7 @@ CONFIGS = {
 }
 
 
-def ncu_traffic(path=ROOT / "profiles" / "r01" / "ncu_lines3d_main.txt"):
+def ncu_traffic(path=ROOT / "profiles" / "r02" / "ncu" / "lines3d_c5.summary.txt"):
     """DRAM bytes (read + write) per launch of the main kernel from the committed
     ncu --set full summary (None when absent)."""
     try:
@@ -393,7 +393,7 @@ def main():
                "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                             "frac": round(achieved / peak, 4),
                             "traffic": ncu_traffic() if plan[0] == "lines" and (H, W, D) == (2048, 2048, 2048) else None,
-                            "traffic_source": "profiles/r01/ncu_lines3d_main.txt (ncu --set full, main launch, "
+                            "traffic_source": "profiles/r02/ncu/lines3d_c5.summary.txt (ncu --set full, one launch, "
                                               "dram__bytes_read + dram__bytes_write)",
                             "kernel": kname + ", per-launch median over CUDA events",
                             "kernel_ms": round(kms, 4), "peak_source": peak_kind,
