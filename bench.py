@@ -66,18 +66,43 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + clock-event (throttle) reasons sampled during the timed
+    region: NVML polled every 5 ms on a thread (nvidia-smi -lms 100 when NVML
+    is unavailable)."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
-    def __init__(self, index):
-        self.index = index
-        self.rows = []
+    def __init__(self, index, uuid=None, period_s=0.005):
+        self.index, self.uuid, self.period = index, uuid, period_s
+        self.rows = []      # (sm_mhz, max_mhz, power_w, {reason names})
         self.proc = None
+        self.nvml = None
+        self._stop = threading.Event()
+
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        h = None
+        if self.uuid:
+            try:
+                h = pynvml.nvmlDeviceGetHandleByUUID(self.uuid)
+            except pynvml.NVMLError:
+                h = None
+        if h is None:
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+        return pynvml, h
 
     def __enter__(self):
+        try:
+            self.nvml = self._nvml_handle()
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return self
+        except Exception:  # noqa: BLE001 -- NVML missing or unusable: fall back
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
@@ -88,28 +113,60 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def _poll(self):
+        nv, h = self.nvml
+        bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                pw = nv.nvmlDeviceGetPowerUsage(h) / 1e3
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((float(sm), float(mx), pw, {n for n, b in bits.items() if r & b}))
+            except nv.NVMLError:
+                pass
+            time.sleep(self.period)
+
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
+            r = [c.strip() for c in line.split(",")]
+            try:
+                self.rows.append((float(r[1]), float(r[2]), float(r[3]),
+                                  {n for n, v in zip(self.NAMES, r[5:9]) if v.lower() == "active"}))
+            except (IndexError, ValueError):
+                pass
 
     def __exit__(self, *exc):
+        self._stop.set()
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+        elif self.nvml:
+            self.thread.join(timeout=1)
         return False
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v.strip().lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        sm = [r[0] for r in self.rows]
+        return {"sm_mhz": statistics.median(sm), "sm_min_mhz": min(sm), "sm_max_mhz": max(r[1] for r in self.rows),
+                "power_w_max": round(max(r[2] for r in self.rows), 1),
+                "reasons": sorted(set().union(*(r[3] for r in self.rows))), "samples": len(self.rows),
+                "source": "nvml 5 ms" if self.nvml else "nvidia-smi 100 ms"}
+
+
+def _gpu_uuid(dev):
+    import torch
+    try:
+        return "GPU-" + str(torch.cuda.get_device_properties(dev).uuid)
+    except Exception:  # noqa: BLE001
+        return None
 
 
 def cpu_model():
@@ -244,17 +301,17 @@ def main():
     hist = kind.new(3, M, dev)
     stream = torch.cuda.current_stream(dev)
     k_start, k_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    kernel_ms = []
 
-    def step(timed_kernel=False):
+    def step(ev=None):
         # the fused curve path: level histograms (ft_lines3d) -> NCCL
-        # all-reduce (N > 1) -> device prefix scan into the three curves
+        # all-reduce (N > 1) -> device prefix scan into the three curves;
+        # ev = (start, end) events around the histogram kernel
         hist.zero_()
-        if timed_kernel:
-            k_start.record(stream)
+        if ev is not None:
+            ev[0].record(stream)
         kind.launch(3, x, shape, M, quant, (a, b), first=r0, hist=hist)
-        if timed_kernel:
-            k_end.record(stream)
+        if ev is not None:
+            ev[1].record(stream)
         if ws > 1:
             import torch.distributed as dist
             dist.all_reduce(hist)
@@ -271,20 +328,19 @@ def main():
     barrier()
     torch.cuda.synchronize()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev.index) as clk:
+    # the dominant kernel's launch durations, measured inside the timed region
+    # (event pairs on the launching stream around every ft_lines3d launch)
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(dev.index, _gpu_uuid(dev)) as clk:
         t0.record(stream)
-        for _ in range(args.steps):
-            step()
+        for i in range(args.steps):
+            step(kev[i])
         t1.record(stream)
         torch.cuda.synchronize()
     barrier()
     ms = t0.elapsed_time(t1) / args.steps
-    # kernel-only durations (dominant kernel, for the roofline), separate pass
-    for _ in range(max(3, args.steps // 2)):
-        step(timed_kernel=True)
-        torch.cuda.synchronize()
-        kernel_ms.append(k_start.elapsed_time(k_end))
-    kms = statistics.median(kernel_ms)
+    kernel_ms = [e0.elapsed_time(e1) for e0, e1 in kev]
+    kms = statistics.mean(kernel_ms)
     t_ms = torch.tensor([ms, kms], dtype=torch.float64, device=dev)
     if ws > 1:
         import torch.distributed as dist
@@ -395,7 +451,7 @@ def main():
                             "traffic": ncu_traffic() if plan[0] == "lines" and (H, W, D) == (2048, 2048, 2048) else None,
                             "traffic_source": "profiles/r02/ncu/lines3d_c5.summary.txt (ncu --set full, one launch, "
                                               "dram__bytes_read + dram__bytes_write)",
-                            "kernel": kname + ", per-launch median over CUDA events",
+                            "kernel": kname + ", mean launch duration over the timed region (CUDA events on the launching stream)",
                             "kernel_ms": round(kms, 4), "peak_source": peak_kind,
                             "algorithmic_bytes_per_launch": int(bytes_per_launch)},
                "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": 2 * args.steps,

@@ -10,19 +10,27 @@ __global__ void lines_sbase_probe(uint32_t* out)
     *out = (uint32_t)__cvta_generic_to_shared(smem_raw);
 }
 
-// The kernels address shared memory absolutely (LINES_SBASE): check once.
+static int g_sbase = -1;  // measured shared base (-1: not probed yet)
+
+// The kernels take their shared base from cvta at run time; the host fit
+// checks (16-bit packed offsets) need its value: probe once.
 int lines_check_sbase()
 {
-    static int state = -1;  // -1 unchecked, FT_OK, or an error code
-    if (state >= 0) return state;
+    if (g_sbase >= 0) return FT_OK;
     uint32_t *d = nullptr, v = 0;
     if (cudaMalloc(&d, 4) != cudaSuccess) return FT_ERR_CUDA_BASE + (int)cudaGetLastError();
     lines_sbase_probe<<<1, 1, 16>>>(d);
     const cudaError_t e = cudaMemcpy(&v, d, 4, cudaMemcpyDeviceToHost);
     cudaFree(d);
     if (e != cudaSuccess) return FT_ERR_CUDA_BASE + (int)e;
-    state = v == LINES_SBASE ? FT_OK : FT_ERR_INTERNAL;
-    return state;
+    g_sbase = (int)v;
+    return FT_OK;
+}
+
+int lines_sbase()
+{
+    if (g_sbase < 0) lines_check_sbase();
+    return g_sbase >= 0 ? g_sbase : (int)LINES_SBASE_DEFAULT;
 }
 
 // The three device quantizers of the fused kernels, run on a flat buffer
@@ -40,7 +48,7 @@ __global__ void quant_probe_kernel(const typename Elem<DT>::T* __restrict__ x, i
         const float Mf = (float)M;
         for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; 2 * i < n; i += stride) {
             const P2 v = reinterpret_cast<const P2*>(x)[i];
-            const uint32_t w = pack_pow2_sat<DT>(v, q.inv, Mf, 4u) - LINES_SB2;
+            const uint32_t w = pack_pow2_sat<DT>(v, q.inv, Mf, 4u, 0u);
             out[2 * i] = (int32_t)((w & 0xFFFFu) >> 2);
             out[2 * i + 1] = (int32_t)(w >> 18);
         }

@@ -7,10 +7,16 @@
 
 namespace ft {
 
-// shared-space address of the dynamic shared memory block of a non-cluster
-// launch (after the 1 KB the hardware reserves); launch_lines3d verifies it
-constexpr uint32_t LINES_SBASE = 0x400;
-constexpr uint32_t LINES_SB2 = LINES_SBASE * 0x10001u;
+// Packed level words carry the shared-space address of the kernel's dynamic
+// shared block in both halves (sb2 = base * 0x10001), read at run time with
+// cvta (lines_sb2); the host-side fit checks use the base the probe kernel
+// measured once per process (lines_sbase: 0x400 on B200, the 1 KB the
+// hardware reserves).
+constexpr uint32_t LINES_SBASE_DEFAULT = 0x400;
+__device__ __forceinline__ uint32_t lines_sb2(const void* smem)
+{
+    return (uint32_t)__cvta_generic_to_shared(smem) * 0x10001u;
+}
 
 // bit 15 / 31 of x as 0 / 255 in each 16-bit half: ONE PRMT (sign-replicate
 // byte 1 / byte 3 into byte 0 / byte 2, zero bytes 1 / 3) instead of a shift
@@ -33,7 +39,8 @@ __device__ __forceinline__ uint32_t cmp2(uint32_t prev, uint32_t cur) { return c
 // ARE the level -- all on the FMA pipes (no F2I: the conversion unit is a
 // quarter-rate pipe on B200).  Levels * 4, packed.
 template <int DT>
-__device__ __forceinline__ uint32_t pack_pow2_sat(const typename Pair<DT>::T& v, float inv, float Mf, uint32_t four)
+__device__ __forceinline__ uint32_t pack_pow2_sat(const typename Pair<DT>::T& v, float inv, float Mf, uint32_t four,
+                                                  uint32_t sb2)
 {
     const float a = __saturatef((float)v.x * inv);
     const float b = __saturatef((float)v.y * inv);
@@ -43,7 +50,7 @@ __device__ __forceinline__ uint32_t pack_pow2_sat(const typename Pair<DT>::T& v,
     unsigned long long y, z;
     asm("fma.rm.f32x2 %0, %1, %2, %3;" : "=l"(y) : "l"(ab), "l"(m2), "l"(0x3F0000003F000000ull));
     asm("add.rm.f32x2 %0, %1, %2;" : "=l"(z) : "l"(y), "l"(0x4B0000004B000000ull));
-    return __byte_perm((uint32_t)z, (uint32_t)(z >> 32), 0x5410) * four + LINES_SB2;  // IMAD: FMA pipe
+    return __byte_perm((uint32_t)z, (uint32_t)(z >> 32), 0x5410) * four + sb2;  // IMAD: FMA pipe
 }
 
 // Shared-memory increments of both 16-bit halves of a packed address.  No
@@ -51,8 +58,8 @@ __device__ __forceinline__ uint32_t pack_pow2_sat(const typename Pair<DT>::T& v,
 // without an event points at a DUMMY word instead (all such lanes hit the
 // same word: one bank access, merged by the POPC increment).  The halves are
 // split on the FMA pipe (IMAD.HI / IMAD), the ALU pipe being the busy one.
-// Packed level words carry the shared address of the block (LINES_SBASE, in
-// every half), so a half IS the shared address of a signature bin and the
+// Packed level words carry the shared address of the block (sb2, in every
+// half), so a half IS the shared address of a signature bin and the
 // plus/minus rows are an immediate above it: ATOMS [R + imm], no base add.
 template <int OFF>
 __device__ __forceinline__ void sinc2(uint32_t addr)
@@ -87,8 +94,11 @@ __device__ __forceinline__ uint32_t ev_sel(uint32_t flags, uint32_t addr, uint32
 constexpr int LINES_MINUS = 32768;      // byte offset of the minus row (bit 15 of a packed address)
 constexpr int LINES_PLUS = 65536;
 
-// Checks once per process that dynamic shared memory starts at LINES_SBASE
-// (the kernels address it absolutely); FT_OK or an error code.
+// Probes once per process where dynamic shared memory starts (the kernels
+// address it absolutely and the 16-bit packed offsets must fit below 64 KB):
+// FT_OK or an error code; lines_sbase() is the measured base (the default
+// until the probe ran).
 int lines_check_sbase();
+int lines_sbase();
 
 }  // namespace ft

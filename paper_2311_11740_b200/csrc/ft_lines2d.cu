@@ -40,14 +40,14 @@ constexpr int L2L_SIG = 15;   // signature rows u + 5 (s + 1)
 template <int DT, int QM, bool VEC, bool EDGE, int PF>
 __device__ __forceinline__ void lines2d_item(const typename Elem<DT>::T* __restrict__ img, const LGeo& g,
                                              const QuantDev& q, const float* __restrict__ tt, int64_t ia,
-                                             int64_t ib, int k0, int lane)
+                                             int64_t ib, int k0, int lane, uint32_t sbw)
 {
     using P2 = typename Pair<DT>::T;
     using T = typename Elem<DT>::T;
     constexpr uint32_t FULL = 0xFFFFFFFFu;
     const int Wi = (int)g.W;
     const uint32_t sent4 = (uint32_t)(g.M + 1) * 4u;
-    const uint32_t S2 = sent4 * 0x10001u + LINES_SB2;
+    const uint32_t S2 = sent4 * 0x10001u + sbw;
     const uint32_t hk = (uint32_t)g.hk;
     const uint32_t ONE = g.one, MONE = 0u - g.one;
     const float Mf = (float)g.M;
@@ -71,9 +71,9 @@ __device__ __forceinline__ void lines2d_item(const typename Elem<DT>::T* __restr
     auto quant_in = [&](const P2& src) -> uint32_t {
         uint32_t v;
         if constexpr (QM == FT_Q_POW2)
-            v = pack_pow2_sat<DT>(src, q.inv, Mf, g.four);
+            v = pack_pow2_sat<DT>(src, q.inv, Mf, g.four, sbw);
         else
-            v = pack_pair<DT, QM, 0>(src, true, true, tt, q, g.M, sent4) + LINES_SB2;
+            v = pack_pair<DT, QM, 0>(src, true, true, tt, q, g.M, sent4) + sbw;
         return EDGE ? sel_mask(lanekeep, v, S2) : v;
     };
     auto quant = [&](int t, const P2& src) -> uint32_t { return t >= t_lo && t < t_hi ? quant_in(src) : S2; };
@@ -193,6 +193,7 @@ __global__ void __launch_bounds__(L2L_NTH, MINB) lines2d_kernel(const typename E
     __syncthreads();
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t sbw = lines_sb2(smem_raw);
     constexpr int NW = L2L_NTH / 32;
     const int64_t nrows = g.v1 - g.v0;
     const int ntiles = g.tiles_k;
@@ -216,9 +217,9 @@ __global__ void __launch_bounds__(L2L_NTH, MINB) lines2d_kernel(const typename E
             if (r0 >= r1) continue;
             const int k0 = t * 62 - 1;
             if (k0 >= 1 && k0 + 63 <= g.W)
-                lines2d_item<DT, QM, VEC, false, PF>(img, g, q, tt, g.v0 + r0, g.v0 + r1, k0, lane);
+                lines2d_item<DT, QM, VEC, false, PF>(img, g, q, tt, g.v0 + r0, g.v0 + r1, k0, lane, sbw);
             else
-                lines2d_item<DT, QM, VEC, true, PF>(img, g, q, tt, g.v0 + r0, g.v0 + r1, k0, lane);
+                lines2d_item<DT, QM, VEC, true, PF>(img, g, q, tt, g.v0 + r0, g.v0 + r1, k0, lane, sbw);
         }
         __syncthreads();
         // fold: C = sum of signature rows, E = sum (4 - u) rows, EC = plus -
@@ -251,8 +252,9 @@ static int lines2d_hs(int M) { return 255 * (int)cdiv(cdiv((int64_t)(M + 2) * 4,
 static bool lines2d_ok(int M)
 {
     const int hs = lines2d_hs(M);
-    return (M + 2) * 4 <= hs && (L2L_SIG - 1) * hs + (M + 1) * 4 + (int)LINES_SBASE < LINES_PLUS &&
-           (M + 1) * 4 + (int)LINES_SBASE < LINES_MINUS && hs + (M + 2) * 4 <= LINES_MINUS;
+    const int sb = lines_sbase();
+    return (M + 2) * 4 <= hs && (L2L_SIG - 1) * hs + (M + 1) * 4 + sb < LINES_PLUS &&
+           (M + 1) * 4 + sb < LINES_MINUS && hs + (M + 2) * 4 <= LINES_MINUS;
 }
 
 template <int DT, int QM>

@@ -76,7 +76,7 @@ __host__ __device__ inline int lines_end(int hs, bool) { return LINES_PLUS + LIN
 template <int DT, int QM, bool VEC, int R, bool FOLD, int DS, int EDGE>
 __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restrict__ buf, const LGeo& g,
                                            const QuantDev& q, const float* __restrict__ tt, char* __restrict__ h,
-                                           int64_t ia, int64_t ib, int j0, int k0, int lane)
+                                           int64_t ia, int64_t ib, int j0, int k0, int lane, uint32_t sbw)
 {
     using P2 = typename Pair<DT>::T;
     using T = typename Elem<DT>::T;
@@ -87,7 +87,7 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
     const int Di = DS > 0 ? DS : (int)g.D;
     const int64_t pe = g.W * (int64_t)Di;
     const uint32_t sent4 = (uint32_t)(g.M + 1) * 4u;
-    const uint32_t S2 = sent4 * 0x10001u + LINES_SB2;  // sentinel level word (with the shared base)
+    const uint32_t S2 = sent4 * 0x10001u + sbw;  // sentinel level word (with the shared base)
     const uint32_t hk = (uint32_t)g.hk;  // signature row stride / 255
     // 1 and -1 as registers ptxas cannot see through: the adds below stay
     // IMADs on the FMA pipe instead of IADD3 on the (saturated) ALU pipe
@@ -148,9 +148,9 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
         for (int r = 0; r < NR; ++r) {
             uint32_t v;
             if constexpr (QM == FT_Q_POW2)
-                v = pack_pow2_sat<DT>(src[r], q.inv, Mf, g.four);
+                v = pack_pow2_sat<DT>(src[r], q.inv, Mf, g.four, sbw);
             else
-                v = pack_pair<DT, QM, 0>(src[r], true, true, tt, q, g.M, sent4) + LINES_SB2;
+                v = pack_pair<DT, QM, 0>(src[r], true, true, tt, q, g.M, sent4) + sbw;
             V[r] = EDGE ? sel_mask(lanekeep, v, S2) : v;
         }
         if constexpr (EDGE == 2) {
@@ -165,9 +165,9 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
             for (int r = 0; r < NR; ++r) {
                 uint32_t v;
                 if constexpr (QM == FT_Q_POW2)
-                    v = pack_pow2_sat<DT>(src[r], q.inv, Mf, g.four);
+                    v = pack_pow2_sat<DT>(src[r], q.inv, Mf, g.four, sbw);
                 else
-                    v = pack_pair<DT, QM, 0>(src[r], true, true, tt, q, g.M, sent4) + LINES_SB2;
+                    v = pack_pair<DT, QM, 0>(src[r], true, true, tt, q, g.M, sent4) + sbw;
                 V[r] = EDGE ? sel_mask(lanekeep, v, S2) : v;
             }
             if constexpr (EDGE == 2) {
@@ -371,16 +371,17 @@ __global__ void __launch_bounds__(LINES_NTH, LINES_MINB) lines3d_kernel(const ty
 
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x / 32;
+    const uint32_t sbw = lines_sb2(smem_raw);
     if constexpr (MODE != 1) {
         // A: interior column tiles; B: the k-boundary ones (EDGE 1 march)
         const int64_t np = g.v1 - g.v0;
         const int ntk = g.tiles_k - g.kb_lo - g.kb_hi;
         cta_tiles<R>(g, ntk, np, warp, [&](int j0, int tk, int64_t ia, int64_t ib) {
-            lines_item<DT, QM, VEC, R, FOLD, DS, 0>(buf, g, q, tt, h, ia, ib, j0, (g.kb_lo + tk) * 62 - 1, lane);
+            lines_item<DT, QM, VEC, R, FOLD, DS, 0>(buf, g, q, tt, h, ia, ib, j0, (g.kb_lo + tk) * 62 - 1, lane, sbw);
         });
         cta_tiles<R>(g, g.kb_lo + g.kb_hi, np, warp, [&](int j0, int tk, int64_t ia, int64_t ib) {
             const int t = tk < g.kb_lo ? tk : g.tiles_k - g.kb_hi + (tk - g.kb_lo);
-            lines_item<DT, QM, VEC, R, FOLD, DS, 1>(buf, g, q, tt, h, ia, ib, j0, t * 62 - 1, lane);
+            lines_item<DT, QM, VEC, R, FOLD, DS, 1>(buf, g, q, tt, h, ia, ib, j0, t * 62 - 1, lane, sbw);
         });
     }
     if constexpr (MODE != 0) {
@@ -395,7 +396,7 @@ __global__ void __launch_bounds__(LINES_NTH, LINES_MINB) lines3d_kernel(const ty
             const int j0 = g.rf_j0[rem - tk * g.rf_n];
             const int64_t ia = g.v0 + ch * g.e_chunk;
             const int64_t ib = min(ia + (int64_t)g.e_chunk, g.v1);
-            lines_item<DT, QM, VEC, R, FOLD, DS, 2>(buf, g, q, tt, h, ia, ib, j0, tk * 62 - 1, lane);
+            lines_item<DT, QM, VEC, R, FOLD, DS, 2>(buf, g, q, tt, h, ia, ib, j0, tk * 62 - 1, lane, sbw);
         }
     }
     __syncthreads();
@@ -426,11 +427,12 @@ static int lines_hs(int M) { return 255 * (int)cdiv(cdiv((int64_t)(M + 2) * 4, 2
 // 16-bit packed signature offsets: (rows - 1) * hs + level * 4 must fit
 static bool lines_fold_ok(int M, int hs)
 {
-    return 20 * hs + (M + 1) * 4 + (int)LINES_SBASE < LINES_PLUS && (M + 2) * 4 <= hs;
+    return 20 * hs + (M + 1) * 4 + lines_sbase() < LINES_PLUS && (M + 2) * 4 <= hs;
 }
 static bool lines_ok(int M)
 {
-    return (M + 1) * 4 + (int)LINES_SBASE < LINES_MINUS && 6 * lines_hs(M) + (M + 1) * 4 + (int)LINES_SBASE < LINES_PLUS &&
+    const int sb = lines_sbase();
+    return (M + 1) * 4 + sb < LINES_MINUS && 6 * lines_hs(M) + (M + 1) * 4 + sb < LINES_PLUS &&
            lines_hs(M) + (M + 2) * 4 <= LINES_MINUS;
 }
 

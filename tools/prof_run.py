@@ -8,6 +8,12 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
+import os  # noqa: E402
+
+if os.environ.get("FT_DEV_LIB"):  # dev A/B only: load a variant build of the library
+    from paper_2311_11740_b200 import _lib, build as _b  # noqa: E402
+    _b.LIB = Path(os.environ["FT_DEV_LIB"]).resolve()
+    _lib.load(build_if_missing=False)
 import paper_2311_11740_b200 as ft  # noqa: E402
 from paper_2311_11740_b200 import engine, synth  # noqa: E402
 
