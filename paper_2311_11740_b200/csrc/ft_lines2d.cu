@@ -29,15 +29,19 @@
 namespace ft {
 
 constexpr int L2L_NTH = 512;  // 16 warps, each a 62-column strip
-constexpr int L2L_RB = 64;    // rows per (row block, column tile) piece
-constexpr int L2L_SIG = 15;   // signature rows u + 5 (s + 1)
+// rows per (row block, column tile) piece (measured 64 / 96 / 128 / 256:
+// profiles/r02/s3/ab_lines2d_rb.log)
+constexpr int L2L_RB = 96;
+constexpr int L2L_SIG = 15;        // signature rows u + 5 (s + 1)
 
 // One warp strip: lattice columns k0 .. k0+61 of one image, lattice rows
 // [ia, ib).  Lane l holds cells (kk, kk+1), kk = k0-1+2l; lane 0 computes its
 // high half, lane 31 its low half (as in ft_lines.cu).  EDGE: columns outside
 // the image (clamped pair loads, masked halves).
-// PF: rows in flight per lane (even: the ping-pong march state).
-template <int DT, int QM, bool VEC, bool EDGE, int PF>
+// PF: rows in flight per lane (even: the ping-pong march state).  WS > 0: the
+// row stride W as a compile-time constant, so the PF row loads of a step are
+// immediate offsets from one pointer (no 64-bit address math per row).
+template <int DT, int QM, bool VEC, bool EDGE, int PF, int WS>
 __device__ __forceinline__ void lines2d_item(const typename Elem<DT>::T* __restrict__ img, const LGeo& g,
                                              const QuantDev& q, const float* __restrict__ tt, int64_t ia,
                                              int64_t ib, int k0, int lane, uint32_t sbw)
@@ -45,7 +49,8 @@ __device__ __forceinline__ void lines2d_item(const typename Elem<DT>::T* __restr
     using P2 = typename Pair<DT>::T;
     using T = typename Elem<DT>::T;
     constexpr uint32_t FULL = 0xFFFFFFFFu;
-    const int Wi = (int)g.W;
+    const int Wi = WS > 0 ? WS : (int)g.W;
+    const int64_t Ws = WS > 0 ? (int64_t)WS : g.W;  // row stride (elements)
     const uint32_t sent4 = (uint32_t)(g.M + 1) * 4u;
     const uint32_t S2 = sent4 * 0x10001u + sbw;
     const uint32_t hk = (uint32_t)g.hk;
@@ -63,7 +68,7 @@ __device__ __forceinline__ void lines2d_item(const typename Elem<DT>::T* __restr
     const bool okx = kk >= 0 && kk < Wi, oky = kk + 1 >= 0 && kk + 1 < Wi;
     const uint32_t lanekeep = (okx ? 0x0000FFFFu : 0u) | (oky ? 0xFFFF0000u : 0u);
     const int kc = !EDGE ? kk : VEC ? min(max(kk, 0), Wi - 2) : min(max(kk, 0), Wi - 1);
-    const T* ptr = img + ((ia - 2 - g.first) * g.W + kc);  // row ia-2 (t = -1)
+    const T* ptr = img + ((ia - 2 - g.first) * Ws + kc);  // row ia-2 (t = -1)
 
     auto fetch = [&](int t, const T* at, P2& dst) {
         if (t >= t_lo && t < tf) dst = load_pair<DT, VEC>(at, true, EDGE ? kk + 1 < Wi : true);
@@ -86,7 +91,7 @@ __device__ __forceinline__ void lines2d_item(const typename Elem<DT>::T* __restr
     {
         P2 r0, r1;
         fetch(-1, ptr, r0);
-        fetch(0, ptr + g.W, r1);
+        fetch(0, ptr + Ws, r1);
         const uint32_t V0 = quant(-1, r0);
         sa.pV = quant(0, r1);
         const uint32_t Wm0 = shift_pair(__shfl_up_sync(FULL, V0, 1), V0);
@@ -97,8 +102,8 @@ __device__ __forceinline__ void lines2d_item(const typename Elem<DT>::T* __restr
         sa.eC = cmp2(C0, sa.pC);
     }
 #pragma unroll
-    for (int p = 0; p < PF; ++p) fetch(p + 1, ptr + (p + 2) * g.W, raw[p]);
-    ptr += (PF + 2) * g.W;  // row t = PF+1
+    for (int p = 0; p < PF; ++p) fetch(p + 1, ptr + (p + 2) * Ws, raw[p]);
+    ptr += (PF + 2) * Ws;  // row t = PF+1
 
     // row t arrives in V; every event of the row before it (state o) is booked
     auto step = [&](uint32_t V, const St& o, St& x) {
@@ -136,27 +141,27 @@ __device__ __forceinline__ void lines2d_item(const typename Elem<DT>::T* __restr
 #pragma unroll
         for (int p = 0; p < PF; ++p) {
             const uint32_t V = quant_in(raw[p]);
-            raw[p] = load_pair<DT, VEC>(ptr + p * g.W, true, EDGE ? kk + 1 < Wi : true);
+            raw[p] = load_pair<DT, VEC>(ptr + p * Ws, true, EDGE ? kk + 1 < Wi : true);
             if (p & 1)
                 step(V, sb, sa);
             else
                 step(V, sa, sb);
         }
-        ptr += PF * g.W;
+        ptr += PF * Ws;
     }
     for (; s < nm; s += PF) {
 #pragma unroll
         for (int p = 0; p < PF; ++p) {
             if (s + p < nm) {
                 const uint32_t V = quant_in(raw[p]);
-                fetch(s + p + PF + 1, ptr + p * g.W, raw[p]);
+                fetch(s + p + PF + 1, ptr + p * Ws, raw[p]);
                 if (p & 1)
                     step(V, sb, sa);
                 else
                     step(V, sa, sb);
             }
         }
-        ptr += PF * g.W;
+        ptr += PF * Ws;
     }
     if (nm < n) {  // at most one step: the absent row H
         if (nm & 1)
@@ -175,7 +180,7 @@ __device__ __forceinline__ void lines2d_item(const typename Elem<DT>::T* __restr
 // PF / MINB: rows in flight per lane / CTAs per SM the registers are
 // budgeted for -- 8 / 1 for single images (latency-bound: more bytes in
 // flight per warp), 4 / 2 for batches (measured, profiles/r01/lines2d_notes.md).
-template <int DT, int QM, bool VEC, int PF, int MINB>
+template <int DT, int QM, bool VEC, int PF, int MINB, int WS>
 __global__ void __launch_bounds__(L2L_NTH, MINB) lines2d_kernel(const typename Elem<DT>::T* __restrict__ buf, LGeo g,
                                                              QuantDev q, unsigned long long* __restrict__ hist)
 {
@@ -217,9 +222,9 @@ __global__ void __launch_bounds__(L2L_NTH, MINB) lines2d_kernel(const typename E
             if (r0 >= r1) continue;
             const int k0 = t * 62 - 1;
             if (k0 >= 1 && k0 + 63 <= g.W)
-                lines2d_item<DT, QM, VEC, false, PF>(img, g, q, tt, g.v0 + r0, g.v0 + r1, k0, lane, sbw);
+                lines2d_item<DT, QM, VEC, false, PF, WS>(img, g, q, tt, g.v0 + r0, g.v0 + r1, k0, lane, sbw);
             else
-                lines2d_item<DT, QM, VEC, true, PF>(img, g, q, tt, g.v0 + r0, g.v0 + r1, k0, lane, sbw);
+                lines2d_item<DT, QM, VEC, true, PF, WS>(img, g, q, tt, g.v0 + r0, g.v0 + r1, k0, lane, sbw);
         }
         __syncthreads();
         // fold: C = sum of signature rows, E = sum (4 - u) rows, EC = plus -
@@ -279,14 +284,20 @@ static int launch_lines2d(const ft_window* win, int64_t H, int64_t W, int64_t v0
     const size_t smem = (size_t)(LINES_PLUS + LINES_MINUS + g.hs);
     using K = void (*)(const T*, LGeo, QuantDev, unsigned long long*);
     const bool single = g.n_items == 1;
-    K kern = single ? (vec ? lines2d_kernel<DT, QM, true, 8, 1> : lines2d_kernel<DT, QM, false, 8, 1>)
-                    : (vec ? lines2d_kernel<DT, QM, true, 4, 2> : lines2d_kernel<DT, QM, false, 4, 2>);
+    K kern = single ? (vec ? lines2d_kernel<DT, QM, true, 8, 1, 0> : lines2d_kernel<DT, QM, false, 8, 1, 0>)
+                    : (vec ? lines2d_kernel<DT, QM, true, 4, 2, 0> : lines2d_kernel<DT, QM, false, 4, 2, 0>);
+    // the BASELINE configs' row lengths (C2: 8192 f32 pow2, C3: 1024 u8
+    // identity) with immediate-offset row loads
+    if constexpr ((DT == FT_F32 && QM == FT_Q_POW2) || (DT == FT_U8 && QM == FT_Q_IDENTITY)) {
+        if (vec && W == 8192) kern = single ? lines2d_kernel<DT, QM, true, 8, 1, 8192> : lines2d_kernel<DT, QM, true, 4, 2, 8192>;
+        if (vec && W == 1024) kern = single ? lines2d_kernel<DT, QM, true, 8, 1, 1024> : lines2d_kernel<DT, QM, true, 4, 2, 1024>;
+    }
     FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     FT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L2L_NTH, smem));
     if (per_sm < 1) return FT_ERR_ARG;
     const int64_t units = g.n_items * cdiv(v1 - v0, (int64_t)L2L_RB) * g.tiles_k * L2L_RB;
-    // >= 16 * 64 units (one piece per warp) per CTA
+    // >= one piece per warp per CTA
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm_l() * per_sm,
                                                                 cdiv(units, (int64_t)(L2L_NTH / 32) * L2L_RB)));
     kern<<<(int)grid, L2L_NTH, smem, st>>>(static_cast<const T*>(win->data), g, qd,
