@@ -89,9 +89,6 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
     const uint32_t sent4 = (uint32_t)(g.M + 1) * 4u;
     const uint32_t S2 = sent4 * 0x10001u + sbw;  // sentinel level word (with the shared base)
     const uint32_t hk = (uint32_t)g.hk;  // signature row stride / 255
-    // 1 and -1 as registers ptxas cannot see through: the adds below stay
-    // IMADs on the FMA pipe instead of IADD3 on the (saturated) ALU pipe
-    const uint32_t ONE = g.one, MONE = 0u - g.one;
     const float Mf = (float)g.M;
     // lane l holds cells kk, kk+1 (kk even: aligned pair loads); lattice
     // columns k0 .. k0+61 are computed by lane 0's high half, both halves of
@@ -192,7 +189,7 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
     // march state of the previous cell plane; two copies, written alternately
     // by the 2-step unrolled march, so no register moves carry it over
     struct St {
-        uint32_t pV[NR], tmi[R + 1], pWm[R + 1];
+        uint32_t pV[NR], pt3[R + 1], pWm[R + 1];  // pt3: the +i term t3 of plane p-2 (tmi = 255 - pt3)
         uint32_t pB[R + 1], eB[R + 1], pC[R + 1], eC[R + 1], pD[R + 1], eD[R + 1];
     };
     St sa, sb2;
@@ -207,7 +204,7 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
         derive(sa.pV, Wm1, C1);
 #pragma unroll
         for (int r = 1; r <= R; ++r) {
-            sa.tmi[r] = hff(cmp2(V0[r], sa.pV[r]));
+            sa.pt3[r] = hff(cmp2(V0[r], sa.pV[r])) ^ FF2;  // plane ia-1's -i neighbour NOT first
             sa.pWm[r] = Wm1[r];
             const uint32_t b0 = vmin2(V0[r - 1], V0[r]), b1 = vmin2(sa.pV[r - 1], sa.pV[r]);
             const uint32_t d0 = vmin2(C0[r - 1], C0[r]), d1 = vmin2(C1[r - 1], C1[r]);
@@ -236,28 +233,30 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
             // signature of the plane-(p-1) cell: "face neighbour n activates
             // first" = bit 15 / 31 of c' - n + k (k = 0 for -side, -1 for +side)
             const uint32_t cb = o.pV[r] | 0x80008000u;
-            const uint32_t cb1 = cb * ONE + 0xFFFEFFFFu;                      // cb - 0x10001
-            const uint32_t t1 = r == 1 ? hff(cb - o.pV[0]) : tpj * MONE + FF2;  // -j
-            const uint32_t t2 = hff(o.pWm[r] * MONE + cb);                      // -k
-            const uint32_t t3 = hff(W_ * MONE + cb1);                           // +i
-            const uint32_t t4 = hff(o.pV[r + 1] * MONE + cb1);                  // +j
+            const uint32_t t2 = hff(cb - o.pWm[r]);                 // -k
+            const uint32_t t3 = hff(cb - W_ - 0x10001u);            // +i
+            const uint32_t t4 = hff(cb - o.pV[r + 1] - 0x10001u);   // +j
+            // -j: row 1 compares with the halo row; row r > 1 is the
+            // complement of row r-1's +j term (t1 = 255 - tpj)
             // +k: "right neighbour first" is the complement of the right
             // neighbour's -k term (lo: this word's hi half, hi: the next lane's lo)
-            const uint32_t t5 = shift_pair(t2, __shfl_down_sync(FULL, t2, 1)) * MONE + FF2;
+            const uint32_t sh5 = shift_pair(t2, __shfl_down_sync(FULL, t2, 1));
             uint32_t evS;
             if constexpr (FOLD) {
-                // row u + 7 (s_i + 1) = (t1 + t2 + t4 + t5) + 14 - 6 (tmi + t3), in
-                // units of 255; no half borrows: 14 - 6 n_i >= 2
-                uint32_t sum = t1 * ONE + 14u * FF2;
-                sum = t2 * ONE + sum;
-                sum = t4 * ONE + sum;
-                sum = t5 * ONE + sum;
-                const uint32_t row = (o.tmi[r] * ONE + t3) * (uint32_t)(-6) + sum;
+                // row u + 7 (s_i + 1) = (t1 + t2 + t4 + t5) + 14 - 6 (tmi + t3) in
+                // units of 255, with t5 = 255 - sh5, tmi = 255 - pt3, t1 as
+                // above: plain packed adds (IADD3), the constants folded.  The
+                // sums are linear and every half ENDS in [0, 20 * 255], so
+                // intermediate cross-half borrows cancel.
+                const uint32_t base = r == 1 ? hff(cb - o.pV[0]) + 9u * FF2 : 10u * FF2 - tpj;
+                const uint32_t row = base + t2 + t4 - sh5 + 6u * (o.pt3[r] - t3);
                 evS = row * hk + o.pV[r];
             } else {
-                evS = (o.tmi[r] + t1 + t2 + t3 + t4 + t5) * hk + o.pV[r];
+                const uint32_t t1 = r == 1 ? hff(cb - o.pV[0]) : FF2 - tpj;
+                const uint32_t tmi = o.pt3[r] ^ FF2;
+                evS = (tmi + t1 + t2 + t3 + t4 + (FF2 - sh5)) * hk + o.pV[r];
                 // A line event iff both or neither i-neighbour is first; minus (max) iff t3
-                const uint32_t fA = ~(o.tmi[r] ^ t3) & lmask;
+                const uint32_t fA = ~(tmi ^ t3) & lmask;
                 const uint32_t aA = o.pV[r] | ((t3 << 8) & 0x80008000u);
                 sinc2<LINES_PLUS>(ev_sel(fA << 8, aA, dummy2));
             }
@@ -270,7 +269,7 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
             sinc2<LINES_PLUS>(ev_sel((o.eB[r] ^ nB) & lmask, o.pB[r] | (nB & 0x80008000u), dummy2));
             sinc2<LINES_PLUS>(ev_sel((o.eC[r] ^ nC) & lmask, o.pC[r] | (nC & 0x80008000u), dummy2));
             sinc2<LINES_PLUS>(ev_sel((o.eD[r] ^ nD) & lmask, o.pD[r] | (~nD & 0x80008000u), dummy2));
-            x.tmi[r] = t3 * MONE + FF2;
+            x.pt3[r] = t3;
             tpj = t4;
             x.pWm[r] = Wm[r];
             x.pB[r] = B;
