@@ -27,7 +27,7 @@ struct LGeo {
     int kb_lo, kb_hi;                // ft_lines3d: k-boundary column tiles at each end
     int e_chunk;                     // ft_lines3d: planes per boundary warp item
     int64_t e_items;                 // ft_lines3d: boundary warp items
-    uint32_t one, four;              // ft_lines3d: 1 and 4 as opaque registers (IMAD, not IADD3/LEA)
+    uint32_t four;                   // line kernels: 4 as an opaque register (the quantizer's IMAD, not LEA)
 };
 
 __device__ __forceinline__ uint32_t vmin2(uint32_t a, uint32_t b) { return __vminu2(a, b); }

@@ -54,7 +54,6 @@ __device__ __forceinline__ void lines2d_item(const typename Elem<DT>::T* __restr
     const uint32_t sent4 = (uint32_t)(g.M + 1) * 4u;
     const uint32_t S2 = sent4 * 0x10001u + sbw;
     const uint32_t hk = (uint32_t)g.hk;
-    const uint32_t ONE = g.one, MONE = 0u - g.one;
     const float Mf = (float)g.M;
     const int kk = k0 - 1 + 2 * lane;
     const uint32_t lmask = __shfl_sync(FULL, lane == 0 ? 0xFFFF0000u : lane == 31 ? 0x0000FFFFu : FULL, lane);
@@ -84,7 +83,7 @@ __device__ __forceinline__ void lines2d_item(const typename Elem<DT>::T* __restr
     auto quant = [&](int t, const P2& src) -> uint32_t { return t >= t_lo && t < t_hi ? quant_in(src) : S2; };
 
     struct St {
-        uint32_t pV, tmi, pWm, pC, eC;
+        uint32_t pV, pt3, pWm, pC, eC;  // pt3: the +i term t3 of the row before (tmi = 255 - pt3)
     };
     St sa, sb;
     P2 raw[PF];  // rows in flight: raw[p] holds row t = p+1 (mod PF)
@@ -98,7 +97,7 @@ __device__ __forceinline__ void lines2d_item(const typename Elem<DT>::T* __restr
         sa.pWm = shift_pair(__shfl_up_sync(FULL, sa.pV, 1), sa.pV);
         const uint32_t C0 = vmin2(V0, Wm0);
         sa.pC = vmin2(sa.pV, sa.pWm);
-        sa.tmi = hff(cmp2(V0, sa.pV));  // the -i neighbour (row ia-2) activates first
+        sa.pt3 = hff(cmp2(V0, sa.pV)) ^ FF2;  // the -i neighbour (row ia-2) does NOT activate first
         sa.eC = cmp2(C0, sa.pC);
     }
 #pragma unroll
@@ -110,21 +109,20 @@ __device__ __forceinline__ void lines2d_item(const typename Elem<DT>::T* __restr
         const uint32_t Wm = shift_pair(__shfl_up_sync(FULL, V, 1), V);
         const uint32_t Cn = vmin2(V, Wm);
         const uint32_t cb = o.pV | 0x80008000u;
-        const uint32_t cb1 = cb * ONE + 0xFFFEFFFFu;  // cb - 0x10001
-        const uint32_t t2 = hff(o.pWm * MONE + cb);   // -j neighbour first
-        const uint32_t t3 = hff(V * MONE + cb1);      // +i neighbour first
+        const uint32_t t2 = hff(cb - o.pWm);            // -j neighbour first
+        const uint32_t t3 = hff(cb - V - 0x10001u);     // +i neighbour first
         // +j: complement of the right neighbour's -j term
-        const uint32_t t5 = shift_pair(t2, __shfl_down_sync(FULL, t2, 1)) * MONE + FF2;
-        // row u + 5 (s + 1) = t2 + t5 + 10 - 4 (tmi + t3), units of 255, >= 2
-        uint32_t sum = t2 * ONE + 10u * FF2;
-        sum = t5 * ONE + sum;
-        const uint32_t row = (o.tmi * ONE + t3) * (uint32_t)(-4) + sum;
+        const uint32_t sh5 = shift_pair(t2, __shfl_down_sync(FULL, t2, 1));
+        // row u + 5 (s + 1) = t2 + t5 + 10 - 4 (tmi + t3) in units of 255, with
+        // t5 = 255 - sh5 and tmi = 255 - pt3: packed adds, constants folded;
+        // every half ends in [0, 14 * 255] (intermediate borrows cancel)
+        const uint32_t row = t2 - sh5 + 4u * (o.pt3 - t3) + 7u * FF2;
         sinc2<0>(sel_mask(lmask, row * hk + o.pV, dummy2));
         // B line (min over columns j-1, j): +1 at a local min (plus row), -1
         // at a local max (minus row)
         const uint32_t nC = cmp2(o.pC, Cn);
         sinc2<LINES_PLUS>(ev_sel((o.eC ^ nC) & lmask, o.pC | (~nC & 0x80008000u), dummy2));
-        x.tmi = t3 * MONE + FF2;
+        x.pt3 = t3;
         x.pWm = Wm;
         x.pC = Cn;
         x.eC = nC;
@@ -272,7 +270,6 @@ static int launch_lines2d(const ft_window* win, int64_t H, int64_t W, int64_t v0
     g.bstride = win->batch_stride;
     g.hs = lines2d_hs(M);
     g.hk = g.hs / 255;
-    g.one = 1;
     g.four = 4;
     g.tiles_k = (int)((W + 1) / 62 + 1);  // tile t: lattice columns 62 t - 1 .. 62 t + 60
     g.n_items = std::max<int64_t>(win->batch, 1);

@@ -513,7 +513,6 @@ static int launch_lines3d(const ft_window* win, int64_t H, int64_t W, int64_t D,
     g.H = H; g.W = W; g.D = D; g.v0 = v0; g.v1 = v1; g.first = win->first; g.M = M;
     g.hs = lines_hs(M);
     g.hk = g.hs / 255;
-    g.one = 1;
     g.four = 4;
     const bool vec = D % 2 == 0 && reinterpret_cast<uintptr_t>(win->data) % (2 * sizeof(T)) == 0;
     const bool fold = lines_fold_ok(M, g.hs);
