@@ -42,7 +42,7 @@ CONFIGS = {
 }
 
 
-def ncu_traffic(path=ROOT / "profiles" / "r02" / "s3f" / "lines3d_c5.summary.txt"):
+def ncu_traffic(path=ROOT / "profiles" / "r02" / "s3g" / "lines3d_c5.summary.txt"):
     """DRAM bytes (read + write) per launch of the main kernel from the committed
     ncu --set full summary (None when absent)."""
     try:
@@ -449,7 +449,7 @@ def main():
                "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                             "frac": round(achieved / peak, 4),
                             "traffic": ncu_traffic() if plan[0] == "lines" and (H, W, D) == (2048, 2048, 2048) else None,
-                            "traffic_source": "profiles/r02/s3f/lines3d_c5.summary.txt (ncu --set full, one launch, "
+                            "traffic_source": "profiles/r02/s3g/lines3d_c5.summary.txt (ncu --set full, one launch, "
                                               "dram__bytes_read + dram__bytes_write)",
                             "kernel": kname + ", mean launch duration over the timed region (CUDA events on the launching stream)",
                             "kernel_ms": round(kms, 4), "peak_source": peak_kind,
