@@ -1,6 +1,6 @@
 """Build A/B variants of the benchmark path's translation unit (ft_lines_f32p.cu:
 f32 / FT_Q_POW2) linked with the other objects of the main build:  python tools/dev/variants.py name="-DX=1 -DY=2" ...
-Each lands in variants/<name>/libfieldtopo_b200.so (use with FT_LIB=...)."""
+Each lands in variants/<name>/libfieldtopo_b200.so (use with FT_DEV_LIB=... python tools/prof_run.py; dev A/B only)."""
 import concurrent.futures as cf
 import subprocess
 import sys
