@@ -111,3 +111,42 @@ def test_lines2d_streaming_and_workers(ft, orc):
     for workers in (1, 3):
         got = ft.descriptor_curves(src, _tabs(ft), workers=workers)
         assert all(np.array_equal(c.numerators, w) for c, w in zip(got, want)), workers
+
+
+@pytest.mark.parametrize("H,W,vr,M,batch", [(97, 8192, (0.0, 1.0), 255, 1), (5, 8192, (0.0, 1.0), 511, 1),
+                                           (200, 1024, (0.0, 1.0), 255, 1), (1, 1024, (0.0, 2.0), 99, 1),
+                                           (33, 1024, (0.0, 1.0), 255, 6)])
+def test_lines2d_stride_specialised_f32(ft, orc, H, W, vr, M, batch):
+    """The compiled-stride kernels (W = 8192 / 1024, f32 power-of-two range;
+    ft_lines2d.cu) on small heights: single images, a batch, row windows of
+    a streamed source -- against the oracle."""
+    import torch
+    from scipy.ndimage import gaussian_filter
+    rng = np.random.default_rng(H + W + batch)
+    x = gaussian_filter(rng.standard_normal((batch, H, W)).astype(np.float32), (0, 2.0, 2.0), mode="wrap")
+    x = ((x - x.min()) / (x.max() - x.min())).astype(np.float32) * np.float32(vr[1])
+    x[0, 0, 3] = -1.0          # clipped to level 0
+    x[0, H - 1, W - 2] = 9.0   # clipped to level M
+    if batch == 1:
+        src = ft.DeviceSource(torch.from_numpy(x[0]).cuda(), M, value_range=vr)
+        got = [ft.descriptor_curves(src, _tabs(ft))]
+        win = ft.descriptor_curves(ft.ArraySource(x[0], M, value_range=vr), _tabs(ft), chunk_bytes=3 * W * 4)
+        assert all(np.array_equal(a.numerators, b.numerators) for a, b in zip(win, got[0]))
+    else:
+        got = ft.descriptor_curves_batch(torch.from_numpy(x).cuda(), M, _tabs(ft), value_range=vr)
+    for b in range(batch):
+        for c, w in zip(got[b], _want(orc, ft, x[b], M, vr)):
+            assert np.array_equal(c.numerators, w), b
+
+
+@pytest.mark.parametrize("H,batch", [(64, 1), (1, 1), (100, 3)])
+def test_lines2d_stride_specialised_u8(ft, orc, H, batch):
+    """W = 1024 u8 identity levels (the C3 kernels) on small stacks."""
+    import torch
+    rng = np.random.default_rng(H * 7 + batch)
+    imgs = rng.integers(0, 256, size=(batch, H, 1024), dtype=np.uint8)
+    got = ft.descriptor_curves_batch(imgs, 255, _tabs(ft)) if batch > 1 else \
+        [ft.descriptor_curves(ft.DeviceSource(torch.from_numpy(imgs[0]).cuda(), 255), _tabs(ft))]
+    for b in range(batch):
+        for c, w in zip(got[b], _want(orc, ft, imgs[b], 255)):
+            assert np.array_equal(c.numerators, w), b
