@@ -408,8 +408,9 @@ def main():
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e = {"value": round(cells / et.item() / 1e9, 4), "unit": "Gvoxels/s",
                "h2d_bytes_per_step": int((r1 - r0) * W * D * 4 * ws), "d2h_bytes_per_step": int(curves.nbytes),
-               "path": "descriptor_curves-equivalent: ArraySource over pinned host memory, 512 MiB chunks, "
-                       "double-buffered H2D overlapped with the kernel, curves to host"}
+               "path": ("fieldtopo.descriptor_curves(ArraySource(pinned host tensor), tables) -- the public call"
+                        if ws == 1 else "per rank: gather.stream_hist over its planes + NCCL all-reduce")
+                       + "; 512 MiB chunks, double-buffered H2D overlapped with the kernel, curves to host"}
         x = None
     box = {"ec": 8, "surface-area": 8 * 2 * (H * W + W * D + H * D), "volume": 8 * H * W * D}
     checks = {"map_kernel_curves_equal": bool(np.array_equal(map_curves, resident)),
