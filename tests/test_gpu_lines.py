@@ -146,3 +146,25 @@ def test_lines_raw_f32_streaming(ft, orc, tmp_path):
                 assert src.value_range == (float(x.min()), float(x.max()))
             got = ft.descriptor_curves(src, _tabs(ft), chunk_bytes=7 * 70 * 130 * 4)
             assert all(np.array_equal(c.numerators, w) for c, w in zip(got, want)), vr
+
+
+@pytest.mark.parametrize("dtype,D,vr,M", [(np.float32, 1024, (0.0, 1.0), 511), (np.float32, 2048, (0.0, 1.0), 511),
+                                          (np.float32, 1024, (0.1, 0.9), 255), (np.float32, 2048, (0.0, 2.0), 1023),
+                                          (np.uint16, 512, (0.0, 65535.0), 1023), (np.uint16, 1024, (0.0, 65535.0), 255),
+                                          (np.uint16, 2048, (0.0, 65535.0), 511)])
+def test_lines_row_length_specialised(ft, orc, dtype, D, vr, M):
+    """The D-specialised instantiations (immediate-offset row loads; 256 /
+    512 / 1024 / 2048 for f32 pow2 + table and u16 table inputs) on fields
+    small enough for the oracle, incl. the k-boundary tiles of those lengths."""
+    import torch
+    x = _grf((11, 70, D), 2.0, D + M)
+    if dtype == np.uint16:
+        x = np.floor(x * 65535 + 0.5).astype(np.uint16)
+    else:
+        x = x * np.float32(vr[1])
+        x[3, 5, D - 1] = -1.0   # clipped to level 0
+        x[7, 69, 0] = 10.0      # clipped to level M
+    src = ft.DeviceSource(torch.from_numpy(x).cuda(), M, value_range=vr)
+    got = ft.descriptor_curves(src, _tabs(ft), path="lines")
+    for c, w in zip(got, _want(orc, ft, x, M, vr)):
+        assert np.array_equal(c.numerators, w)
