@@ -18,6 +18,32 @@ namespace ft {
 
 constexpr int kSMs = 148;
 
+// ------------------------------------------------ opt-in shared-memory checks
+// compute-sanitizer is unavailable on the GPU pool, so a build with
+// -DFT_BOUNDS_CHECK (tools/dev/build_checked.py) traps on any shared-memory
+// histogram update outside its block: ft_sh_add checks a row index against
+// the histogram's extent, ft_check_smem an absolute shared-window address
+// (the line kernels' packed 16-bit addresses) against the dynamic block.
+// The product build compiles both to the bare atomic.
+#ifdef FT_BOUNDS_CHECK
+__device__ __forceinline__ void ft_check_smem(uint32_t addr)
+{
+    extern __shared__ unsigned char ft_dyn_smem_chk[];
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(ft_dyn_smem_chk);
+    uint32_t size;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(size));
+    if (addr < base || addr + 4u > base + size || (addr & 3u)) __trap();
+}
+__device__ __forceinline__ void ft_sh_add(uint32_t* h, uint32_t i, uint32_t n)
+{
+    if (i >= n) __trap();
+    atomicAdd(&h[i], 1u);
+}
+#else
+__device__ __forceinline__ void ft_check_smem(uint32_t) {}
+__device__ __forceinline__ void ft_sh_add(uint32_t* h, uint32_t i, uint32_t) { atomicAdd(&h[i], 1u); }
+#endif
+
 // ------------------------------------------------------------------ loads
 template <int DT> struct Elem;
 template <> struct Elem<FT_I32> { using T = int32_t; };

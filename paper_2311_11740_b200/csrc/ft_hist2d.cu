@@ -139,8 +139,8 @@ __device__ __forceinline__ void hm_item(const typename Elem<DT>::T* __restrict__
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             const uint32_t x = (w[e] & vmask) | (dummy & ~vmask);
-            atomicAdd(&h[x & 0xFFFFu], 1u);
-            atomicAdd(&h[x >> 16], 1u);
+            ft_sh_add(h, x & 0xFFFFu, 7u * M2);
+            ft_sh_add(h, x >> 16, 7u * M2);
         }
         a = u0 - 2u * K1;
         c = u1 - 2u * K1;

@@ -136,25 +136,25 @@ __device__ __forceinline__ void book3_pair(uint32_t* __restrict__ h, const uint3
     const uint32_t ib = ((k[4] & S7) << 9) | ((k[5] & S7) << 6) | ((k[6] & S7) << 3) | (k[7] & S7);
     if (lo) {
         const uint32_t ea = ta[ia & 0xFFFu], eb = tb[ib & 0xFFFu];
-        atomicAdd(&h[(k[0] & 0xFFFFu) >> 3], 1u);
-        atomicAdd(&h[(ea & 0xFFu) * M2 + ((k[1] & 0xFFFFu) >> 3)], 1u);
-        atomicAdd(&h[((ea >> 8) & 0xFFu) * M2 + ((k[2] & 0xFFFFu) >> 3)], 1u);
-        atomicAdd(&h[(ea >> 16) * M2 + ((k[3] & 0xFFFFu) >> 3)], 1u);
-        atomicAdd(&h[(eb & 0xFFu) * M2 + ((k[4] & 0xFFFFu) >> 3)], 1u);
-        atomicAdd(&h[((eb >> 8) & 0xFFu) * M2 + ((k[5] & 0xFFFFu) >> 3)], 1u);
-        atomicAdd(&h[(eb >> 16) * M2 + ((k[6] & 0xFFFFu) >> 3)], 1u);
-        atomicAdd(&h[39u * M2 + ((k[7] & 0xFFFFu) >> 3)], 1u);
+        ft_sh_add(h, (k[0] & 0xFFFFu) >> 3, NROW3 * M2);
+        ft_sh_add(h, (ea & 0xFFu) * M2 + ((k[1] & 0xFFFFu) >> 3), NROW3 * M2);
+        ft_sh_add(h, ((ea >> 8) & 0xFFu) * M2 + ((k[2] & 0xFFFFu) >> 3), NROW3 * M2);
+        ft_sh_add(h, (ea >> 16) * M2 + ((k[3] & 0xFFFFu) >> 3), NROW3 * M2);
+        ft_sh_add(h, (eb & 0xFFu) * M2 + ((k[4] & 0xFFFFu) >> 3), NROW3 * M2);
+        ft_sh_add(h, ((eb >> 8) & 0xFFu) * M2 + ((k[5] & 0xFFFFu) >> 3), NROW3 * M2);
+        ft_sh_add(h, (eb >> 16) * M2 + ((k[6] & 0xFFFFu) >> 3), NROW3 * M2);
+        ft_sh_add(h, 39u * M2 + ((k[7] & 0xFFFFu) >> 3), NROW3 * M2);
     }
     if (hi) {
         const uint32_t ea = ta[ia >> 16], eb = tb[ib >> 16];
-        atomicAdd(&h[k[0] >> 19], 1u);
-        atomicAdd(&h[(ea & 0xFFu) * M2 + (k[1] >> 19)], 1u);
-        atomicAdd(&h[((ea >> 8) & 0xFFu) * M2 + (k[2] >> 19)], 1u);
-        atomicAdd(&h[(ea >> 16) * M2 + (k[3] >> 19)], 1u);
-        atomicAdd(&h[(eb & 0xFFu) * M2 + (k[4] >> 19)], 1u);
-        atomicAdd(&h[((eb >> 8) & 0xFFu) * M2 + (k[5] >> 19)], 1u);
-        atomicAdd(&h[(eb >> 16) * M2 + (k[6] >> 19)], 1u);
-        atomicAdd(&h[39u * M2 + (k[7] >> 19)], 1u);
+        ft_sh_add(h, k[0] >> 19, NROW3 * M2);
+        ft_sh_add(h, (ea & 0xFFu) * M2 + (k[1] >> 19), NROW3 * M2);
+        ft_sh_add(h, ((ea >> 8) & 0xFFu) * M2 + (k[2] >> 19), NROW3 * M2);
+        ft_sh_add(h, (ea >> 16) * M2 + (k[3] >> 19), NROW3 * M2);
+        ft_sh_add(h, (eb & 0xFFu) * M2 + (k[4] >> 19), NROW3 * M2);
+        ft_sh_add(h, ((eb >> 8) & 0xFFu) * M2 + (k[5] >> 19), NROW3 * M2);
+        ft_sh_add(h, (eb >> 16) * M2 + (k[6] >> 19), NROW3 * M2);
+        ft_sh_add(h, 39u * M2 + (k[7] >> 19), NROW3 * M2);
     }
 }
 

@@ -40,6 +40,8 @@ __device__ __forceinline__ uint32_t shift_pair(uint32_t a, uint32_t b) { return 
 __device__ __forceinline__ void inc2(char* __restrict__ h, int row, int hs, uint32_t w)
 {
     char* base = h + row * hs;
+    ft_check_smem((uint32_t)__cvta_generic_to_shared(base + (w & 0xFFFFu)));
+    ft_check_smem((uint32_t)__cvta_generic_to_shared(base + (w >> 16)));
     atomicAdd(reinterpret_cast<uint32_t*>(base + (w & 0xFFFFu)), 1u);
     atomicAdd(reinterpret_cast<uint32_t*>(base + (w >> 16)), 1u);
 }

@@ -66,6 +66,8 @@ __device__ __forceinline__ void sinc2(uint32_t addr)
 {
     const uint32_t hi = __umulhi(addr, 0x10000u);
     const uint32_t lo = addr - hi * 0x10000u;
+    ft_check_smem(lo + OFF);
+    ft_check_smem(hi + OFF);
     asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(lo), "n"(OFF));
     asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(hi), "n"(OFF));
 }
