@@ -214,6 +214,11 @@ def cpu_reference(x_host, M, lo_hi, descs, budget_s=15.0, threads=None):
         n = min(H, n * 2)
         t = run(n)
     n_final = max(min(H, 4 * threads), min(H, int(n * budget_s / max(t, 1e-6))))
+    # the reference split hands the remainder rows to the LAST worker
+    # (_parallel.py:19-23): a sample that is a multiple of the thread count
+    # keeps its threads evenly loaded (110 rows on 16 threads would leave 20
+    # to the last one and time the reference ~3x too slow)
+    n_final = max(threads, n_final - n_final % threads) if n_final > threads else n_final
     t, maps = run(n_final), last[0]
     cells = n_final * W * D
     return cells / t / 1e9, cells, t, threads, n_final, maps

@@ -28,6 +28,7 @@
 namespace ft {
 
 constexpr int NTAB = 4096;            // rank-group table entries
+constexpr int NXT = 512;              // XOR-relative rank-group table entries
 // Classification failures (the reference raises ValueError "3D neighborhood
 // outside the configuration table", contrib3d.py:304-305/330, re-raised as
 // ClassificationError, contrib3d.py:425-426): table entries of impossible
@@ -41,6 +42,7 @@ struct Geo3 {
     int64_t H, W, D, v0, v1, first;
     int M;
     int tiles_j, tiles_k;
+    uint32_t c8;  // 8, as a run-time value (Book3)
 };
 
 // Class ids of ranks (1,2,3) indexed by the first four sorted slots, and of
@@ -48,6 +50,14 @@ struct Geo3 {
 struct RankTables {
     uint32_t a[NTAB];
     uint32_t b[NTAB];
+    // The pair classes only see XORs of slots (contrib3d.py:76-90), so a rank
+    // group's classes are invariant under s -> s ^ c: xa is indexed by the
+    // first four sorted slots relative to the first, (s1^s0, s2^s0, s3^s0), xb
+    // by the last four relative to the last, (s6^s7, s5^s7, s4^s7) -- 512
+    // entries each, small enough to keep one copy PER LANE in shared memory
+    // (entry e of lane l at word 32 e + l: bank l, no conflicts).
+    uint32_t xa[NXT];
+    uint32_t xb[NXT];
 };
 
 template <int DT, int QM>
@@ -59,19 +69,29 @@ __device__ __forceinline__ uint32_t level3(const typename Elem<DT>::T* __restric
                             q.negate, g.M);
 }
 
-__device__ __forceinline__ uint32_t slot_index(uint32_t a, uint32_t b, uint32_t c, uint32_t d)
+__host__ __device__ __forceinline__ uint32_t slot_index(uint32_t a, uint32_t b, uint32_t c, uint32_t d)
 {
     return ((a & 7u) << 9) | ((b & 7u) << 6) | ((c & 7u) << 3) | (d & 7u);
 }
 
+// XT: lane-replicated XOR-relative tables (32 x NXT words each); otherwise the
+// two NTAB-entry absolute tables.
+template <bool XT>
 __device__ __forceinline__ void init_shared3(uint32_t* h, uint32_t* ta, uint32_t* tb, float* tt,
                                              const RankTables* __restrict__ rt, const QuantDev& q, int M2,
                                              bool table)
 {
     for (int i = threadIdx.x; i < NROW3 * M2; i += blockDim.x) h[i] = 0;
-    for (int i = threadIdx.x; i < NTAB; i += blockDim.x) {
-        ta[i] = rt->a[i];
-        tb[i] = rt->b[i];
+    if constexpr (XT) {
+        for (int i = threadIdx.x; i < NXT * 32; i += blockDim.x) {
+            ta[i] = rt->xa[i >> 5];
+            tb[i] = rt->xb[i >> 5];
+        }
+    } else {
+        for (int i = threadIdx.x; i < NTAB; i += blockDim.x) {
+            ta[i] = rt->a[i];
+            tb[i] = rt->b[i];
+        }
     }
     if (table)
         for (int i = threadIdx.x; i < M2; i += blockDim.x) tt[i] = q.tt[i];
@@ -125,54 +145,88 @@ __device__ __forceinline__ void merge44x2(uint32_t* k)
 constexpr int HMR = 4;          // vertex rows per warp strip
 constexpr int HM3_NTH = 512;    // 16 warps: 64 vertex rows per CTA tile
 
-// book3 for a packed vertex pair: the rank-group slot indices of both halves
-// in one pass (12 bits each), levels extracted per half.
-__device__ __forceinline__ void book3_pair(uint32_t* __restrict__ h, const uint32_t* __restrict__ ta,
-                                           const uint32_t* __restrict__ tb, const uint32_t (&k)[8], uint32_t M2,
-                                           bool lo, bool hi)
+// Shared-window addresses of the booking step.  Measured on B200 (profiles/
+// r02/s5/NOTES.md): the ALU pipe (LOP3 / SHF / LEA / PRMT / VIMNMX, half rate)
+// is this kernel's busiest, but IMAD.HI as a right shift is slower than SHF,
+// so shifts stay shifts; the class byte of a table entry is selected,
+// multiplied by the row stride and added to the level offset by ONE IDP.2A.
+struct Book3 {
+    uint32_t hb2;      // 2 x shared address of the histogram in both halves: carried by every key
+    uint32_t r39;      // 39 S: row 39 is the fixed class of rank 7
+    uint32_t ta, tb;   // shared addresses of the rank tables (XT: + 4 lane)
+    uint32_t S, S16;   // row stride in bytes, 4 (M + 2) (< 2^16), and S << 16
+    uint32_t c8;       // 8 as a run-time value: x * c8 + y stays an IMAD
+};
+
+__device__ __forceinline__ void sh_inc(uint32_t addr)
 {
-    constexpr uint32_t S7 = 0x00070007u;
-    const uint32_t ia = ((k[0] & S7) << 9) | ((k[1] & S7) << 6) | ((k[2] & S7) << 3) | (k[3] & S7);
-    const uint32_t ib = ((k[4] & S7) << 9) | ((k[5] & S7) << 6) | ((k[6] & S7) << 3) | (k[7] & S7);
-    if (lo) {
-        const uint32_t ea = ta[ia & 0xFFFu], eb = tb[ib & 0xFFFu];
-        ft_sh_add(h, (k[0] & 0xFFFFu) >> 3, NROW3 * M2);
-        ft_sh_add(h, (ea & 0xFFu) * M2 + ((k[1] & 0xFFFFu) >> 3), NROW3 * M2);
-        ft_sh_add(h, ((ea >> 8) & 0xFFu) * M2 + ((k[2] & 0xFFFFu) >> 3), NROW3 * M2);
-        ft_sh_add(h, (ea >> 16) * M2 + ((k[3] & 0xFFFFu) >> 3), NROW3 * M2);
-        ft_sh_add(h, (eb & 0xFFu) * M2 + ((k[4] & 0xFFFFu) >> 3), NROW3 * M2);
-        ft_sh_add(h, ((eb >> 8) & 0xFFu) * M2 + ((k[5] & 0xFFFFu) >> 3), NROW3 * M2);
-        ft_sh_add(h, (eb >> 16) * M2 + ((k[6] & 0xFFFFu) >> 3), NROW3 * M2);
-        ft_sh_add(h, 39u * M2 + ((k[7] & 0xFFFFu) >> 3), NROW3 * M2);
-    }
-    if (hi) {
-        const uint32_t ea = ta[ia >> 16], eb = tb[ib >> 16];
-        ft_sh_add(h, k[0] >> 19, NROW3 * M2);
-        ft_sh_add(h, (ea & 0xFFu) * M2 + (k[1] >> 19), NROW3 * M2);
-        ft_sh_add(h, ((ea >> 8) & 0xFFu) * M2 + (k[2] >> 19), NROW3 * M2);
-        ft_sh_add(h, (ea >> 16) * M2 + (k[3] >> 19), NROW3 * M2);
-        ft_sh_add(h, (eb & 0xFFu) * M2 + (k[4] >> 19), NROW3 * M2);
-        ft_sh_add(h, ((eb >> 8) & 0xFFu) * M2 + (k[5] >> 19), NROW3 * M2);
-        ft_sh_add(h, (eb >> 16) * M2 + (k[6] >> 19), NROW3 * M2);
-        ft_sh_add(h, 39u * M2 + (k[7] >> 19), NROW3 * M2);
-    }
+    ft_check_smem(addr);
+    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ uint32_t sh_ld(uint32_t addr)
+{
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
 }
 
-template <int DT, int QM, bool VEC, bool EDGE>
+// book3 for a packed vertex pair: the rank-group slot indices of both halves
+// in one pass, one table lookup per rank group and half, eight increments per
+// vertex.  Keys are level * 8 + slot + 2 hb per half (hb = the histogram's
+// shared address, a multiple of 4, so order and slot bits are untouched):
+// with the slot bits cleared the high half's kc >> 17 -- and the low half's
+// (kc << 16) >> 17 -- IS the shared address of the level's bin in row 0.
+template <bool XT>
+__device__ __forceinline__ void book3_pair(const Book3& x, const uint32_t (&k)[8], bool lo, bool hi)
+{
+    constexpr uint32_t S7 = 0x00070007u, LV = 0xFFF8FFF8u;
+    constexpr int SX = XT ? 9 : 14;  // index in the high half -> table byte offset (XT: * 128, else * 4)
+    uint32_t pa, pb;
+    if constexpr (XT) {
+        const uint32_t a1 = (k[1] ^ k[0]) & S7, a2 = (k[2] ^ k[0]) & S7, a3 = (k[3] ^ k[0]) & S7;
+        const uint32_t b1 = (k[6] ^ k[7]) & S7, b2 = (k[5] ^ k[7]) & S7, b3 = (k[4] ^ k[7]) & S7;
+        pa = (a1 * x.c8 + a2) * x.c8 + a3;  // 9 bits per half
+        pb = (b1 * x.c8 + b2) * x.c8 + b3;
+    } else {
+        pa = (((k[0] & S7) * x.c8 + (k[1] & S7)) * x.c8 + (k[2] & S7)) * x.c8 + (k[3] & S7);  // 12 bits per half
+        pb = (((k[4] & S7) * x.c8 + (k[5] & S7)) * x.c8 + (k[6] & S7)) * x.c8 + (k[7] & S7);
+    }
+    uint32_t kc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) kc[e] = k[e] & LV;
+    auto book = [&](uint32_t ea, uint32_t eb, const uint32_t(&t)[8]) {
+        // t[e]: the key of rank e in the HIGH half; class bytes 0..2 of ea / eb
+        // select the rows of ranks 1..3 / 4..6 (IDP.2A: S * byte + address)
+        sh_inc(t[0] >> 17);
+        sh_inc(__dp2a_lo(x.S, ea, t[1] >> 17));
+        sh_inc(__dp2a_lo(x.S16, ea, t[2] >> 17));
+        sh_inc(__dp2a_hi(x.S, ea, t[3] >> 17));
+        sh_inc(__dp2a_lo(x.S, eb, t[4] >> 17));
+        sh_inc(__dp2a_lo(x.S16, eb, t[5] >> 17));
+        sh_inc(__dp2a_hi(x.S, eb, t[6] >> 17));
+        sh_inc((t[7] >> 17) + x.r39);
+    };
+    if (lo) {
+        uint32_t t[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) t[e] = kc[e] << 16;
+        book(sh_ld(((pa << 16) >> SX) + x.ta), sh_ld(((pb << 16) >> SX) + x.tb), t);
+    }
+    if (hi) book(sh_ld((pa >> SX) + x.ta), sh_ld((pb >> SX) + x.tb), kc);
+}
+
+template <int DT, int QM, bool VEC, bool EDGE, bool XT>
 __device__ __forceinline__ void hm3_item(const typename Elem<DT>::T* __restrict__ buf, const Geo3& g,
-                                         const QuantDev& q, const float* __restrict__ tt,
-                                         uint32_t* __restrict__ h, const uint32_t* __restrict__ ta,
-                                         const uint32_t* __restrict__ tb, int64_t ia, int64_t ib, int j0, int k0,
-                                         int lane)
+                                         const QuantDev& q, const float* __restrict__ tt, const Book3& bk,
+                                         int64_t ia, int64_t ib, int j0, int k0, int lane)
 {
     using P2 = typename Pair<DT>::T;
     using T = typename Elem<DT>::T;
     constexpr int NR = HMR + 1;  // cell rows j0-1 .. j0+HMR-1
     constexpr uint32_t FULL = 0xFFFFFFFFu, K1 = 0x10001u;
     const int Wi = (int)g.W, Di = (int)g.D;
-    const uint32_t M2 = (uint32_t)g.M + 2u;
     const uint32_t sent8 = ((uint32_t)g.M + 1u) * 8u;
-    const uint32_t S = sent8 * K1;
+    const uint32_t S = sent8 * K1 + bk.hb2;  // keys carry 2 hb (book3_pair)
     const int kk = k0 - 1 + 2 * lane;
     const bool clo = lane != 0 && kk >= 0 && kk <= Di, chi = lane != 31 && kk + 1 >= 0 && kk + 1 <= Di;
     const bool okx = kk >= 0 && kk < Di, oky = kk + 1 >= 0 && kk + 1 < Di;
@@ -206,7 +260,7 @@ __device__ __forceinline__ void hm3_item(const typename Elem<DT>::T* __restrict_
         const bool exists = t >= t_lo && t < t_hi;
 #pragma unroll
         for (int c = 0; c < NR; ++c) {
-            uint32_t v = pack_pair<DT, QM, 1>(src[c], !EDGE || okx, !EDGE || oky, tt, q, g.M, sent8);
+            uint32_t v = pack_pair<DT, QM, 1>(src[c], !EDGE || okx, !EDGE || oky, tt, q, g.M, sent8) + bk.hb2;
             if (EDGE && !((rowok >> c) & 1u)) v = S;
             V[c] = exists ? v : S;
             Wm[c] = shift_pair(__shfl_up_sync(FULL, V[c], 1), V[c]);
@@ -242,7 +296,7 @@ __device__ __forceinline__ void hm3_item(const typename Elem<DT>::T* __restrict_
             keys4(V, Wm, v, 1u, u);
             uint32_t k8[8] = {prev[v][0], prev[v][1], prev[v][2], prev[v][3], u[0], u[1], u[2], u[3]};
             merge44x2(k8);
-            book3_pair(h, ta, tb, k8, M2, vrow[v] && clo, vrow[v] && chi);
+            book3_pair<XT>(bk, k8, vrow[v] && clo, vrow[v] && chi);
 #pragma unroll
             for (int e = 0; e < 4; ++e) prev[v][e] = u[e] - K1;
         }
@@ -260,7 +314,7 @@ __device__ __forceinline__ void hm3_item(const typename Elem<DT>::T* __restrict_
     }
 }
 
-template <int DT, int QM, bool VEC>
+template <int DT, int QM, bool VEC, bool XT>
 __global__ void __launch_bounds__(HM3_NTH, 1) hist3d_march(const typename Elem<DT>::T* __restrict__ buf, Geo3 g,
                                                           QuantDev q, const RankTables* __restrict__ rt,
                                                           unsigned long long* __restrict__ hist)
@@ -269,11 +323,23 @@ __global__ void __launch_bounds__(HM3_NTH, 1) hist3d_march(const typename Elem<D
     const int M2 = g.M + 2;
     uint32_t* h = reinterpret_cast<uint32_t*>(smem_raw);
     uint32_t* ta = h + NROW3 * M2;
-    uint32_t* tb = ta + NTAB;
-    float* tt = reinterpret_cast<float*>(tb + NTAB);
-    init_shared3(h, ta, tb, tt, rt, q, M2, QM != FT_Q_IDENTITY && QM != FT_Q_POW2);
+    uint32_t* tb = ta + (XT ? NXT * 32 : NTAB);
+    float* tt = reinterpret_cast<float*>(tb + (XT ? NXT * 32 : NTAB));
+    init_shared3<XT>(h, ta, tb, tt, rt, q, M2, QM != FT_Q_IDENTITY && QM != FT_Q_POW2);
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    Book3 bk;
+    // 16-bit keys: level * 8 + slot + 2 hb (hb = 0x400 on B200; the launcher
+    // keeps M + 1 <= 4095, so hb up to ~16 KB would still fit)
+    const uint32_t hb = (uint32_t)__cvta_generic_to_shared(h);
+    if (2u * hb + 8u * (uint32_t)M2 > 0xFFFFu) __trap();
+    bk.hb2 = 2u * hb * 0x10001u;
+    bk.S = 4u * (uint32_t)M2;
+    bk.S16 = bk.S << 16;
+    bk.r39 = 39u * bk.S;
+    bk.ta = (uint32_t)__cvta_generic_to_shared(ta) + (XT ? 4u * lane : 0u);
+    bk.tb = (uint32_t)__cvta_generic_to_shared(tb) + (XT ? 4u * lane : 0u);
+    bk.c8 = g.c8;
     constexpr int TJ = (HM3_NTH / 32) * HMR;
     const int64_t np = g.v1 - g.v0;
     const int64_t T = (int64_t)g.tiles_j * g.tiles_k * np;  // (tile, plane) units, tile-major
@@ -289,9 +355,9 @@ __global__ void __launch_bounds__(HM3_NTH, 1) hist3d_march(const typename Elem<D
         if (j0 > g.W) continue;
         const int64_t ia = g.v0 + p;
         if (j0 >= 1 && j0 + HMR <= g.W && k0 >= 1 && k0 + 63 <= g.D)
-            hm3_item<DT, QM, VEC, false>(buf, g, q, tt, h, ta, tb, ia, ia + len, j0, k0, lane);
+            hm3_item<DT, QM, VEC, false, XT>(buf, g, q, tt, bk, ia, ia + len, j0, k0, lane);
         else
-            hm3_item<DT, QM, VEC, true>(buf, g, q, tt, h, ta, tb, ia, ia + len, j0, k0, lane);
+            hm3_item<DT, QM, VEC, true, XT>(buf, g, q, tt, bk, ia, ia + len, j0, k0, lane);
     }
     __syncthreads();
     flush_hist(h, hist, M2);
@@ -372,6 +438,22 @@ static RankTables make_rank_tables()
         }
         rt.b[idx] = eb;
     }
+    // XOR-relative tables; an entry whose class triple is NOT the same for
+    // every base slot (cannot happen: the pair classes only see XORs) is left
+    // as the trap class, so a broken invariance would fail loudly.
+    for (int idx = 0; idx < NXT; ++idx) {
+        const int x1 = idx >> 6 & 7, x2 = idx >> 3 & 7, x3 = idx & 7;
+        rt.xa[idx] = rt.xb[idx] = TRAP * 0x010101u;
+        if (!x1 || !x2 || !x3 || x1 == x2 || x1 == x3 || x2 == x3) continue;
+        const uint32_t ea = rt.a[slot_index(0, x1, x2, x3)], eb = rt.b[slot_index(x3, x2, x1, 0)];
+        bool same = true;
+        for (int c = 1; c < 8; ++c)
+            same &= rt.a[slot_index(c, x1 ^ c, x2 ^ c, x3 ^ c)] == ea && rt.b[slot_index(x3 ^ c, x2 ^ c, x1 ^ c, c)] == eb;
+        if (same) {
+            rt.xa[idx] = ea;
+            rt.xb[idx] = eb;
+        }
+    }
     return rt;
 }
 
@@ -399,8 +481,14 @@ static const RankTables* device_rank_tables()
 }
 
 // shared bytes of hist3d_march: the 40 x (M+2) histogram, both rank tables, the threshold table
-static size_t march3_smem(int M) { return (size_t)(NROW3 * (M + 2) + 2 * NTAB + (M + 2)) * 4; }
-static bool march3_ok(int M) { return M + 1 <= 8190 && march3_smem(M) <= 227 * 1024; }
+static size_t march3_smem(int M, bool xt) { return (size_t)(NROW3 * (M + 2) + 2 * (xt ? NXT * 32 : NTAB) + (M + 2)) * 4; }
+static bool march3_ok(int M) { return M + 1 <= 4095 && march3_smem(M, false) <= 227 * 1024; }
+// the lane-replicated tables (128 KB) beside the histogram: M <= ~600
+#ifdef HM3_FORCE_NOXT
+static bool march3_xt(int) { return false; }
+#else
+static bool march3_xt(int M) { return march3_smem(M, true) <= 227 * 1024; }
+#endif
 
 template <int DT, int QM>
 static int launch3(const ft_window* win, int64_t H, int64_t W, int64_t D, int64_t v0, int64_t v1,
@@ -418,9 +506,12 @@ static int launch3(const ft_window* win, int64_t H, int64_t W, int64_t D, int64_
     const int nsm = sm_count();
     if (march3_ok(M)) {
         // register march: every vertex (j, k) in [0, W] x [0, D]
-        const size_t sm = march3_smem(M);
+        const bool xt = march3_xt(M);
+        const size_t sm = march3_smem(M, xt);
         const bool vec = D % 2 == 0 && reinterpret_cast<uintptr_t>(buf) % (2 * sizeof(T)) == 0;
-        auto kern = vec ? hist3d_march<DT, QM, true> : hist3d_march<DT, QM, false>;
+        auto kern = xt ? (vec ? hist3d_march<DT, QM, true, true> : hist3d_march<DT, QM, false, true>)
+                       : (vec ? hist3d_march<DT, QM, true, false> : hist3d_march<DT, QM, false, false>);
+        g.c8 = 8;
         FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         int per_sm = 0;
         FT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, HM3_NTH, sm));
@@ -465,6 +556,7 @@ extern "C" int ft_debug_trap_tables(int32_t on)
     static const RankTables bad = [] {
         RankTables r = make_rank_tables();
         for (int i = 0; i < NTAB; ++i) r.a[i] = r.b[i] = TRAP * 0x010101u;
+        for (int i = 0; i < NXT; ++i) r.xa[i] = r.xb[i] = TRAP * 0x010101u;
         return r;
     }();
     FT_CUDA_TRY(cudaMemcpy(const_cast<RankTables*>(d), on ? &bad : &good, sizeof(RankTables), cudaMemcpyHostToDevice));
