@@ -43,6 +43,20 @@ __device__ __forceinline__ void ft_sh_add(uint32_t* h, uint32_t i, uint32_t n)
 __device__ __forceinline__ void ft_check_smem(uint32_t) {}
 __device__ __forceinline__ void ft_sh_add(uint32_t* h, uint32_t i, uint32_t) { atomicAdd(&h[i], 1u); }
 #endif
+// increment / load at an absolute shared-window address (the map kernels'
+// keys carry the histogram's shared address, so a bin address is a mask or a
+// shift of the sorted key)
+__device__ __forceinline__ void ft_sh_inc(uint32_t addr)
+{
+    ft_check_smem(addr);
+    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ uint32_t ft_sh_ld(uint32_t addr)
+{
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
 
 // ------------------------------------------------------------------ loads
 template <int DT> struct Elem;

@@ -87,10 +87,15 @@ __device__ __forceinline__ void hm_cswap2(uint32_t& a, uint32_t& b)
     a = lo;
 }
 
-template <int DT, int QM, bool VEC, bool EDGE>
+// BA (7 rows of byte offsets + the shared base fit 16 bits: M <= ~2260):
+// keys are level * 4 + slot + hb per half, hb = the histogram's shared address
+// (a multiple of 4: order and slot bits untouched), so a key with its slot
+// bits masked IS the shared address of the level's bin in row 0 -- no shift,
+// no index -> address arithmetic.  Otherwise 16-bit word indices.
+template <int DT, int QM, bool VEC, bool EDGE, bool BA>
 __device__ __forceinline__ void hm_item(const typename Elem<DT>::T* __restrict__ img, const Geo2& g,
                                         const QuantDev& q, const float* __restrict__ tt, uint32_t* __restrict__ h,
-                                        int64_t ia, int64_t ib, int k0, int lane)
+                                        uint32_t hb, int64_t ia, int64_t ib, int k0, int lane)
 {
     using P2 = typename Pair<DT>::T;
     using T = typename Elem<DT>::T;
@@ -98,12 +103,13 @@ __device__ __forceinline__ void hm_item(const typename Elem<DT>::T* __restrict__
     const int Wi = (int)g.W;
     const uint32_t M2 = (uint32_t)g.M + 2u;
     const uint32_t sent4 = ((uint32_t)g.M + 1u) * 4u;
-    const uint32_t S = sent4 * K1;
+    const uint32_t hbK = BA ? hb * K1 : 0u;
+    const uint32_t S = sent4 * K1 + hbK;
     const int kk = k0 - 1 + 2 * lane;
     // vertex columns kk (low half) and kk+1 (high half) that this lane books
     const bool vlo = lane != 0 && kk >= 0 && kk <= Wi, vhi = lane != 31 && kk + 1 >= 0 && kk + 1 <= Wi;
     const uint32_t vmask = __shfl_sync(FULL, (vlo ? 0x0000FFFFu : 0u) | (vhi ? 0xFFFF0000u : 0u), lane);
-    const uint32_t dummy = 6u * M2 * K1;
+    const uint32_t dummy = BA ? (hb + 24u * M2) * K1 : 6u * M2 * K1;
     const bool okx = kk >= 0 && kk < Wi, oky = kk + 1 >= 0 && kk + 1 < Wi;
     const int kc = !EDGE ? kk : VEC ? min(max(kk, 0), Wi - 2) : min(max(kk, 0), Wi - 1);
     const int n = (int)(ib - ia);
@@ -117,7 +123,7 @@ __device__ __forceinline__ void hm_item(const typename Elem<DT>::T* __restrict__
         if (t >= t_lo && t < tf) dst = load_pair<DT, VEC>(at, true, EDGE ? kk + 1 < Wi : true);
     };
     auto quant_in = [&](const P2& src) -> uint32_t {
-        return pack_pair<DT, QM, 0>(src, !EDGE || okx, !EDGE || oky, tt, q, g.M, sent4);
+        return pack_pair<DT, QM, 0>(src, !EDGE || okx, !EDGE || oky, tt, q, g.M, sent4) + hbK;
     };
     // one vertex row: sorted NW / NE keys of the row above in a, c
     uint32_t a, c;
@@ -131,16 +137,29 @@ __device__ __forceinline__ void hm_item(const typename Elem<DT>::T* __restrict__
         hm_cswap2(s1, s2);
         // class rows: s0 -> 0, s1 -> 1 (2 if diagonal), s2 -> 3 (4), s3 -> 5
         const uint32_t diag = ((((s0 ^ s1) & 0x00030003u) + K1) >> 2) & K1;  // 1 per half iff slots {0,3} / {1,2}
-        const uint32_t i0 = (s0 >> 2) & 0x3FFF3FFFu;
-        const uint32_t i1 = ((s1 >> 2) & 0x3FFF3FFFu) + (K1 + diag) * M2;
-        const uint32_t i2 = ((s2 >> 2) & 0x3FFF3FFFu) + (3u * K1 + diag) * M2;
-        const uint32_t i3 = ((s3 >> 2) & 0x3FFF3FFFu) + 5u * M2 * K1;
-        const uint32_t w[4] = {i0, i1, i2, i3};
+        if constexpr (BA) {
+            constexpr uint32_t LM = 0xFFFCFFFCu;
+            const uint32_t Sb = 4u * M2;  // row stride in bytes
+            const uint32_t w[4] = {s0 & LM, (s1 & LM) + (K1 + diag) * Sb, (s2 & LM) + (3u * K1 + diag) * Sb,
+                                   (s3 & LM) + 5u * Sb * K1};
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const uint32_t x = (w[e] & vmask) | (dummy & ~vmask);
-            ft_sh_add(h, x & 0xFFFFu, 7u * M2);
-            ft_sh_add(h, x >> 16, 7u * M2);
+            for (int e = 0; e < 4; ++e) {
+                const uint32_t x = (w[e] & vmask) | (dummy & ~vmask);
+                ft_sh_inc(x & 0xFFFFu);
+                ft_sh_inc(x >> 16);
+            }
+        } else {
+            const uint32_t i0 = (s0 >> 2) & 0x3FFF3FFFu;
+            const uint32_t i1 = ((s1 >> 2) & 0x3FFF3FFFu) + (K1 + diag) * M2;
+            const uint32_t i2 = ((s2 >> 2) & 0x3FFF3FFFu) + (3u * K1 + diag) * M2;
+            const uint32_t i3 = ((s3 >> 2) & 0x3FFF3FFFu) + 5u * M2 * K1;
+            const uint32_t w[4] = {i0, i1, i2, i3};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const uint32_t x = (w[e] & vmask) | (dummy & ~vmask);
+                ft_sh_add(h, x & 0xFFFFu, 7u * M2);
+                ft_sh_add(h, x >> 16, 7u * M2);
+            }
         }
         a = u0 - 2u * K1;
         c = u1 - 2u * K1;
@@ -184,7 +203,7 @@ __device__ __forceinline__ void hm_item(const typename Elem<DT>::T* __restrict__
     if (nm < n) step(S);  // vertex row H: the absent row below
 }
 
-template <int DT, int QM, bool VEC>
+template <int DT, int QM, bool VEC, bool BA>
 __global__ void __launch_bounds__(HM_NTH, 2) hist2d_march(const typename Elem<DT>::T* __restrict__ buf, Geo2 g,
                                                          QuantDev q, unsigned long long* __restrict__ hist)
 {
@@ -197,6 +216,8 @@ __global__ void __launch_bounds__(HM_NTH, 2) hist2d_march(const typename Elem<DT
         for (int i = threadIdx.x; i < M2; i += blockDim.x) tt[i] = q.tt[i];
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t hb = (uint32_t)__cvta_generic_to_shared(h);
+    if (BA && hb + 28u * (uint32_t)M2 > 0xFFFFu) __trap();  // the launcher leaves 2 KB for the base
     constexpr int NW = HM_NTH / 32;
     const int64_t nrows = g.v1 - g.v0;
     const int ntiles = g.tiles;
@@ -218,9 +239,9 @@ __global__ void __launch_bounds__(HM_NTH, 2) hist2d_march(const typename Elem<DT
             if (r0 >= r1) continue;
             const int k0 = t * 62 - 1;
             if (k0 >= 1 && k0 + 63 <= g.W)
-                hm_item<DT, QM, VEC, false>(img, g, q, tt, h, g.v0 + r0, g.v0 + r1, k0, lane);
+                hm_item<DT, QM, VEC, false, BA>(img, g, q, tt, h, hb, g.v0 + r0, g.v0 + r1, k0, lane);
             else
-                hm_item<DT, QM, VEC, true>(img, g, q, tt, h, g.v0 + r0, g.v0 + r1, k0, lane);
+                hm_item<DT, QM, VEC, true, BA>(img, g, q, tt, h, hb, g.v0 + r0, g.v0 + r1, k0, lane);
         }
         __syncthreads();
         unsigned long long* out = hist + b * FT_NCLASS_2D * M2;
@@ -259,7 +280,13 @@ static int launch2(const ft_window* win, int64_t H, int64_t W, int64_t v0, int64
         // register march: every vertex column 0..W
         const bool vec = W % 2 == 0 && (g.batch <= 1 || g.bstride % 2 == 0) &&
                          reinterpret_cast<uintptr_t>(buf) % (2 * sizeof(T)) == 0;
-        auto kern = vec ? hist2d_march<DT, QM, true> : hist2d_march<DT, QM, false>;
+#ifdef HM2_NO_BA
+        const bool ba = false;
+#else
+        const bool ba = 28 * M2 + 2048 <= 0xFFFF;  // byte addresses in the 16-bit halves (M <= 2265)
+#endif
+        auto kern = ba ? (vec ? hist2d_march<DT, QM, true, true> : hist2d_march<DT, QM, false, true>)
+                       : (vec ? hist2d_march<DT, QM, true, false> : hist2d_march<DT, QM, false, false>);
         const size_t sm = (size_t)8 * M2 * 4;
         FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         int per_sm = 0;

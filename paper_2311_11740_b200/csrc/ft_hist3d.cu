@@ -158,18 +158,6 @@ struct Book3 {
     uint32_t c8;       // 8 as a run-time value: x * c8 + y stays an IMAD
 };
 
-__device__ __forceinline__ void sh_inc(uint32_t addr)
-{
-    ft_check_smem(addr);
-    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
-}
-__device__ __forceinline__ uint32_t sh_ld(uint32_t addr)
-{
-    uint32_t v;
-    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
-    return v;
-}
-
 // book3 for a packed vertex pair: the rank-group slot indices of both halves
 // in one pass, one table lookup per rank group and half, eight increments per
 // vertex.  Keys are level * 8 + slot + 2 hb per half (hb = the histogram's
@@ -197,22 +185,22 @@ __device__ __forceinline__ void book3_pair(const Book3& x, const uint32_t (&k)[8
     auto book = [&](uint32_t ea, uint32_t eb, const uint32_t(&t)[8]) {
         // t[e]: the key of rank e in the HIGH half; class bytes 0..2 of ea / eb
         // select the rows of ranks 1..3 / 4..6 (IDP.2A: S * byte + address)
-        sh_inc(t[0] >> 17);
-        sh_inc(__dp2a_lo(x.S, ea, t[1] >> 17));
-        sh_inc(__dp2a_lo(x.S16, ea, t[2] >> 17));
-        sh_inc(__dp2a_hi(x.S, ea, t[3] >> 17));
-        sh_inc(__dp2a_lo(x.S, eb, t[4] >> 17));
-        sh_inc(__dp2a_lo(x.S16, eb, t[5] >> 17));
-        sh_inc(__dp2a_hi(x.S, eb, t[6] >> 17));
-        sh_inc((t[7] >> 17) + x.r39);
+        ft_sh_inc(t[0] >> 17);
+        ft_sh_inc(__dp2a_lo(x.S, ea, t[1] >> 17));
+        ft_sh_inc(__dp2a_lo(x.S16, ea, t[2] >> 17));
+        ft_sh_inc(__dp2a_hi(x.S, ea, t[3] >> 17));
+        ft_sh_inc(__dp2a_lo(x.S, eb, t[4] >> 17));
+        ft_sh_inc(__dp2a_lo(x.S16, eb, t[5] >> 17));
+        ft_sh_inc(__dp2a_hi(x.S, eb, t[6] >> 17));
+        ft_sh_inc((t[7] >> 17) + x.r39);
     };
     if (lo) {
         uint32_t t[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) t[e] = kc[e] << 16;
-        book(sh_ld(((pa << 16) >> SX) + x.ta), sh_ld(((pb << 16) >> SX) + x.tb), t);
+        book(ft_sh_ld(((pa << 16) >> SX) + x.ta), ft_sh_ld(((pb << 16) >> SX) + x.tb), t);
     }
-    if (hi) book(sh_ld((pa >> SX) + x.ta), sh_ld((pb >> SX) + x.tb), kc);
+    if (hi) book(ft_sh_ld((pa >> SX) + x.ta), ft_sh_ld((pb >> SX) + x.tb), kc);
 }
 
 template <int DT, int QM, bool VEC, bool EDGE, bool XT>
