@@ -57,15 +57,18 @@ __device__ __forceinline__ uint32_t pack_pow2_sat(const typename Pair<DT>::T& v,
 // predicates: ptxas turns predicated shared atomics into branches, so a lane
 // without an event points at a DUMMY word instead (all such lanes hit the
 // same word: one bank access, merged by the POPC increment).  The halves are
-// split on the FMA pipe (IMAD.HI / IMAD), the ALU pipe being the busy one.
+// split on the FMA pipe, the ALU pipe being the busy one, by two IDP.2A
+// (addr.h0 * b0 + addr.h1 * b1 with (b0, b1) = (1, 0) / (0, 1)): the earlier
+// IMAD.HI / IMAD pair cost 4.4 % of the C5 kernel (IMAD.HI is a slow
+// instruction on B200; profiles/r02/s5/NOTES.md).
 // Packed level words carry the shared address of the block (sb2, in every
 // half), so a half IS the shared address of a signature bin and the
 // plus/minus rows are an immediate above it: ATOMS [R + imm], no base add.
 template <int OFF>
 __device__ __forceinline__ void sinc2(uint32_t addr)
 {
-    const uint32_t hi = __umulhi(addr, 0x10000u);
-    const uint32_t lo = addr - hi * 0x10000u;
+    const uint32_t hi = __dp2a_lo(addr, 0x0100u, 0u);
+    const uint32_t lo = __dp2a_lo(addr, 0x0001u, 0u);
     ft_check_smem(lo + OFF);
     ft_check_smem(hi + OFF);
     asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(lo), "n"(OFF));
