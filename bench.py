@@ -6,9 +6,9 @@ z-slab partitioned over N GPUs with one NCCL all-reduce of the histograms).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1)
 
-One step = one pass of the hot path over the whole field: fused quantize +
-2x2x2 transition-class histogram kernel on this rank's z-slab (+1 halo
-plane), NCCL all-reduce of the histogram (N > 1), device finalize into the
+One step = one pass of the hot path over the whole field: the fused quantize +
+line-decomposition histogram kernel (ft_lines3d) on this rank's z-slab (+2
+halo planes), NCCL all-reduce of the histogram (N > 1), device scan into the
 three curves.  ``value`` is whole-job Gvoxels/s with the field resident in HBM
 (max over ranks of the CUDA-event time); ``e2e`` is the same through the public
 API (``descriptor_curves`` on an ``ArraySource`` over PINNED HOST memory:
@@ -42,7 +42,10 @@ CONFIGS = {
 }
 
 
-def ncu_traffic(path=ROOT / "profiles" / "r02" / "s3g" / "lines3d_c5.summary.txt"):
+NCU_C5 = "profiles/r02/s5/evidence/lines3d_c5.summary.txt"  # latest ncu --set full capture of the C5 kernel
+
+
+def ncu_traffic(path=ROOT / NCU_C5):
     """DRAM bytes (read + write) per launch of the main kernel from the committed
     ncu --set full summary (None when absent)."""
     try:
@@ -455,7 +458,7 @@ def main():
                "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                             "frac": round(achieved / peak, 4),
                             "traffic": ncu_traffic() if plan[0] == "lines" and (H, W, D) == (2048, 2048, 2048) else None,
-                            "traffic_source": "profiles/r02/s3g/lines3d_c5.summary.txt (ncu --set full, one launch, "
+                            "traffic_source": NCU_C5 + " (ncu --set full, one launch, "
                                               "dram__bytes_read + dram__bytes_write)",
                             "kernel": kname + ", mean launch duration over the timed region (CUDA events on the launching stream)",
                             "kernel_ms": round(kms, 4), "peak_source": peak_kind,
