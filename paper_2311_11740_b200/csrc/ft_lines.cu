@@ -4,35 +4,6 @@
 
 namespace ft {
 
-__global__ void lines_sbase_probe(uint32_t* out)
-{
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    *out = (uint32_t)__cvta_generic_to_shared(smem_raw);
-}
-
-static int g_sbase = -1;  // measured shared base (-1: not probed yet)
-
-// The kernels take their shared base from cvta at run time; the host fit
-// checks (16-bit packed offsets) need its value: probe once.
-int lines_check_sbase()
-{
-    if (g_sbase >= 0) return FT_OK;
-    uint32_t *d = nullptr, v = 0;
-    if (cudaMalloc(&d, 4) != cudaSuccess) return FT_ERR_CUDA_BASE + (int)cudaGetLastError();
-    lines_sbase_probe<<<1, 1, 16>>>(d);
-    const cudaError_t e = cudaMemcpy(&v, d, 4, cudaMemcpyDeviceToHost);
-    cudaFree(d);
-    if (e != cudaSuccess) return FT_ERR_CUDA_BASE + (int)e;
-    g_sbase = (int)v;
-    return FT_OK;
-}
-
-int lines_sbase()
-{
-    if (g_sbase < 0) lines_check_sbase();
-    return g_sbase >= 0 ? g_sbase : (int)LINES_SBASE_DEFAULT;
-}
-
 // The three device quantizers of the fused kernels, run on a flat buffer
 // (verification hook for the exhaustive quantizer tests): path 0 to_level
 // (ft_quantize, hist/wide kernels), 1 to_level4 (march / lattice kernels,

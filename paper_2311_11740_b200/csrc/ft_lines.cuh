@@ -1,23 +1,19 @@
 // ft_lines.cuh -- device helpers shared by the line-decomposition curve
-// kernels (ft_lines.cu: 3D, ft_lines2d.cu: 2D): packed 16-bit level words that
-// carry the shared base of the histogram block, the FMA-pipe quantizer, the
-// dummy-address shared increments.
+// kernels (ft_lines.cu: 3D, ft_lines2d.cu: 2D): packed 16-bit bin offsets, the
+// FMA-pipe quantizer, the dummy-address shared increments, the shared layout.
 #pragma once
 #include "ft_lattice.cuh"
 
 namespace ft {
 
-// Packed level words carry the shared-space address of the kernel's dynamic
-// shared block in both halves (sb2 = base * 0x10001), read at run time with
-// cvta (lines_sb2); the host-side fit checks use the base the probe kernel
-// measured once per process (lines_sbase: 0x400 on B200, the 1 KB the
-// hardware reserves).
-constexpr uint32_t LINES_SBASE_DEFAULT = 0x400;
-__device__ __forceinline__ uint32_t lines_sb2(const void* smem)
-{
-    return (uint32_t)__cvta_generic_to_shared(smem) * 0x10001u;
-}
-
+// Packed level words hold, per 16-bit half, the bin's offset BELOW the top of
+// its histogram region: rel = row * hs + (level + 1) * 4 (rel = 0 is the
+// region's dummy word).  The regions are laid out downward (lines_layout), so
+// the shared address of a bin is top - rel and ONE IDP.2A per half does the
+// half split, the event select and the address:
+//     addr = top + h0 * b0 + h1 * b1,   (b0, b1) signed bytes, -1 or 0
+// -- a half whose flag byte is 0 lands on the dummy word at top (sinc2).
+constexpr uint32_t LINES_REL0 = 0x00040004u;  // rel of level 0 in row 0, both halves
 // bit 15 / 31 of x as 0 / 255 in each 16-bit half: ONE PRMT (sign-replicate
 // byte 1 / byte 3 into byte 0 / byte 2, zero bytes 1 / 3) instead of a shift
 // and a mask -- the signature counts run in units of 255 (row stride 255 K).
@@ -53,26 +49,37 @@ __device__ __forceinline__ uint32_t pack_pow2_sat(const typename Pair<DT>::T& v,
     return __byte_perm((uint32_t)z, (uint32_t)(z >> 32), 0x5410) * four + sb2;  // IMAD: FMA pipe
 }
 
-// Shared-memory increments of both 16-bit halves of a packed address.  No
-// predicates: ptxas turns predicated shared atomics into branches, so a lane
-// without an event points at a DUMMY word instead (all such lanes hit the
-// same word: one bank access, merged by the POPC increment).  The halves are
-// split on the FMA pipe, the ALU pipe being the busy one, by two IDP.2A
-// (addr.h0 * b0 + addr.h1 * b1 with (b0, b1) = (1, 0) / (0, 1)): the earlier
-// IMAD.HI / IMAD pair cost 4.4 % of the C5 kernel (IMAD.HI is a slow
-// instruction on B200; profiles/r02/s5/NOTES.md).
-// Packed level words carry the shared address of the block (sb2, in every
-// half), so a half IS the shared address of a signature bin and the
-// plus/minus rows are an immediate above it: ATOMS [R + imm], no base add.
-template <int OFF>
-__device__ __forceinline__ void sinc2(uint32_t addr)
+// Shared-memory increments of both 16-bit halves of a packed word of bin
+// offsets.  No predicates (ptxas turns predicated shared atomics into
+// branches): sel holds a flag byte per half, byte 0 for the low half and byte
+// 3 for the high one (0xFF = book the bin, 0 = no event: the dummy word at
+// top; all such lanes hit the same word, one bank access merged by the POPC
+// increment), bytes 1 and 2 zero.  The two IDP.2A run on the FMA pipe, the ALU
+// pipe being the busy one; an earlier IMAD.HI + IMAD split cost 4.4 % of the
+// C5 kernel (IMAD.HI is a slow instruction on B200; profiles/r02/s5/NOTES.md).
+__device__ __forceinline__ void sinc2(uint32_t rel2, uint32_t sel, uint32_t top)
 {
-    const uint32_t hi = __dp2a_lo(addr, 0x0100u, 0u);
-    const uint32_t lo = __dp2a_lo(addr, 0x0001u, 0u);
-    ft_check_smem(lo + OFF);
-    ft_check_smem(hi + OFF);
-    asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(lo), "n"(OFF));
-    asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(hi), "n"(OFF));
+    uint32_t lo, hi;
+    asm("dp2a.lo.u32.s32 %0, %1, %2, %3;" : "=r"(lo) : "r"(rel2), "r"(sel), "r"(top));
+    asm("dp2a.hi.u32.s32 %0, %1, %2, %3;" : "=r"(hi) : "r"(rel2), "r"(sel), "r"(top));
+    ft_check_smem(lo);
+    ft_check_smem(hi);
+    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(lo));
+    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(hi));
+}
+// sinc2 selector of a lane's dense event: every half it computes (lane 0 only
+// its high half, lane 31 only its low one: the others are the halo cells)
+__device__ __forceinline__ uint32_t lane_sel(int lane)
+{
+    return lane == 0 ? 0xFF000000u : lane == 31 ? 0x000000FFu : 0xFF0000FFu;
+}
+// sinc2 selector from event flags in bits 15 / 31: ONE PRMT (sign-replicate
+// byte 1 into byte 0 and byte 3 into byte 3, zero bytes 1 and 2)
+__device__ __forceinline__ uint32_t ev_sel(uint32_t flags)
+{
+    uint32_t m;
+    asm("prmt.b32 %0, %1, 0, 0xB449;" : "=r"(m) : "r"(flags));
+    return m;
 }
 // (a & m) | (b & ~m) as ONE LOP3 (left to itself ptxas sometimes splits it
 // into two around a hoisted b & ~m)
@@ -82,28 +89,33 @@ __device__ __forceinline__ uint32_t sel_mask(uint32_t m, uint32_t a, uint32_t b)
     asm("lop3.b32 %0, %1, %2, %3, 0xCA;" : "=r"(d) : "r"(m), "r"(a), "r"(b));
     return d;
 }
-// halves of addr whose flag bit (15 / 31) is set, dummy2's halves elsewhere
-__device__ __forceinline__ uint32_t ev_sel(uint32_t flags, uint32_t addr, uint32_t dummy2)
+// Shared layout of the line kernels (byte offsets from the dynamic block),
+// every region growing DOWNWARD from its top:
+//   signature bins (row s, level l) at dtop - (s hs + (l + 1) 4), the dense
+//     dummy word at dtop;
+//   minus-row bins at ptop - 32768 - (l + 1) 4 (bit 15 of a sparse offset
+//     selects the minus row), just above dtop;
+//   plus-row bins at ptop - (l + 1) 4, the sparse dummy word at ptop;
+//   the threshold table in the gap above the minus row.
+// 16-bit halves: (nsig - 1) hs + (M + 2) 4 < 65536 and 2 (M + 2) 4 <= 32768.
+constexpr int LINES_MINUS = 32768;
+struct LLay {
+    int dtop, ptop, tt, end;
+};
+__host__ __device__ inline LLay lines_layout(int hs, int nsig, int M)
 {
-    // sign of byte 1 / byte 3 -> 0xFFFF / 0 per half (PTX prmt sign-replicate
-    // mode; the __byte_perm intrinsic masks the selector to 3 bits)
-    uint32_t m;
-    asm("prmt.b32 %0, %1, 0, 0xBB99;" : "=r"(m) : "r"(flags));
-    return sel_mask(m, addr, dummy2);
+    const int m4 = (M + 2) * 4;
+    LLay L;
+    L.dtop = ((nsig - 1) * hs + m4 + 15) & ~15;
+    L.ptop = (L.dtop + 16 + LINES_MINUS + m4 + 15) & ~15;
+    L.tt = L.ptop - LINES_MINUS;
+    L.end = L.ptop + 16;
+    return L;
 }
-
-// Shared layout of the line kernels: signature rows at 0 (at most 64 KB: the
-// 16-bit packed row offsets), the plus row at LINES_PLUS and the minus row
-// LINES_MINUS above it; both are constants, so every ATOMS address is
-// [R + imm].
-constexpr int LINES_MINUS = 32768;      // byte offset of the minus row (bit 15 of a packed address)
-constexpr int LINES_PLUS = 65536;
-
-// Probes once per process where dynamic shared memory starts (the kernels
-// address it absolutely and the 16-bit packed offsets must fit below 64 KB):
-// FT_OK or an error code; lines_sbase() is the measured base (the default
-// until the probe ran).
-int lines_check_sbase();
-int lines_sbase();
+__host__ __device__ inline bool lines_layout_ok(int hs, int nsig, int M)
+{
+    const int m4 = (M + 2) * 4;
+    return m4 <= hs && (nsig - 1) * hs + m4 < 65536 && 2 * m4 <= LINES_MINUS;
+}
 
 }  // namespace ft

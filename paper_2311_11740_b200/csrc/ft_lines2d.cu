@@ -43,8 +43,8 @@ constexpr int L2L_SIG = 15;        // signature rows u + 5 (s + 1)
 // immediate offsets from one pointer (no 64-bit address math per row).
 template <int DT, int QM, bool VEC, bool EDGE, int PF, int WS>
 __device__ __forceinline__ void lines2d_item(const typename Elem<DT>::T* __restrict__ img, const LGeo& g,
-                                             const QuantDev& q, const float* __restrict__ tt, int64_t ia,
-                                             int64_t ib, int k0, int lane, uint32_t sbw)
+                                             const QuantDev& q, const float* __restrict__ tt, uint32_t topd_u,
+                                             uint32_t topp_u, int64_t ia, int64_t ib, int k0, int lane)
 {
     using P2 = typename Pair<DT>::T;
     using T = typename Elem<DT>::T;
@@ -52,12 +52,15 @@ __device__ __forceinline__ void lines2d_item(const typename Elem<DT>::T* __restr
     const int Wi = WS > 0 ? WS : (int)g.W;
     const int64_t Ws = WS > 0 ? (int64_t)WS : g.W;  // row stride (elements)
     const uint32_t sent4 = (uint32_t)(g.M + 1) * 4u;
+    constexpr uint32_t sbw = LINES_REL0;  // packed words: (level + 1) * 4 per half
     const uint32_t S2 = sent4 * 0x10001u + sbw;
     const uint32_t hk = (uint32_t)g.hk;
     const float Mf = (float)g.M;
     const int kk = k0 - 1 + 2 * lane;
     const uint32_t lmask = __shfl_sync(FULL, lane == 0 ? 0xFFFF0000u : lane == 31 ? 0x0000FFFFu : FULL, lane);
-    const uint32_t dummy2 = S2;
+    const uint32_t lsel = __shfl_sync(FULL, lane_sel(lane), lane);  // dense events: halo halves -> the dummy word
+    // the region tops as per-lane registers (as uniform values ptxas puts a move in front of every IDP)
+    const uint32_t topd = __shfl_sync(FULL, topd_u, lane), topp = __shfl_sync(FULL, topp_u, lane);
     const int n = (int)(ib - ia);
     // rows t = -1 .. n (row ia-1+t) exist iff t_lo <= t < t_hi; rows t < tf
     // are fetched (a window holds rows ia-2 .. ib-1)
@@ -117,11 +120,11 @@ __device__ __forceinline__ void lines2d_item(const typename Elem<DT>::T* __restr
         // t5 = 255 - sh5 and tmi = 255 - pt3: packed adds, constants folded;
         // every half ends in [0, 14 * 255] (intermediate borrows cancel)
         const uint32_t row = t2 - sh5 + 4u * (o.pt3 - t3) + 7u * FF2;
-        sinc2<0>(sel_mask(lmask, row * hk + o.pV, dummy2));
+        sinc2(row * hk + o.pV, lsel, topd);
         // B line (min over columns j-1, j): +1 at a local min (plus row), -1
         // at a local max (minus row)
         const uint32_t nC = cmp2(o.pC, Cn);
-        sinc2<LINES_PLUS>(ev_sel((o.eC ^ nC) & lmask, o.pC | (~nC & 0x80008000u), dummy2));
+        sinc2(o.pC | (~nC & 0x80008000u), ev_sel((o.eC ^ nC) & lmask), topp);
         x.pt3 = t3;
         x.pWm = Wm;
         x.pC = Cn;
@@ -186,17 +189,18 @@ __global__ void __launch_bounds__(L2L_NTH, MINB) lines2d_kernel(const typename E
     char* h = reinterpret_cast<char*>(smem_raw);
     const int M2 = g.M + 2;
     const int hs = g.hs;
-    const int end = LINES_PLUS + LINES_MINUS + hs;
-    float* tt = reinterpret_cast<float*>(h + LINES_PLUS + hs);
+    const LLay lay = lines_layout(hs, L2L_SIG, g.M);
+    float* tt = reinterpret_cast<float*>(h + lay.tt);
     uint32_t* hw = reinterpret_cast<uint32_t*>(h);
-    for (int i = threadIdx.x; i < end / 4; i += blockDim.x) hw[i] = 0;
+    for (int i = threadIdx.x; i < lay.end / 4; i += blockDim.x) hw[i] = 0;
     __syncthreads();
     if (QM != FT_Q_IDENTITY && QM != FT_Q_POW2)
         for (int i = threadIdx.x; i < M2; i += blockDim.x) tt[i] = q.tt[i];
     __syncthreads();
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t sbw = lines_sb2(smem_raw);
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    const uint32_t topd = sb + (uint32_t)lay.dtop, topp = sb + (uint32_t)lay.ptop;
     constexpr int NW = L2L_NTH / 32;
     const int64_t nrows = g.v1 - g.v0;
     const int ntiles = g.tiles_k;
@@ -204,7 +208,8 @@ __global__ void __launch_bounds__(L2L_NTH, MINB) lines2d_kernel(const typename E
     const int64_t batch = g.n_items;  // images
     const int64_t total = batch * Timg;
     const int64_t U0 = total * blockIdx.x / gridDim.x, U1 = total * (blockIdx.x + 1) / gridDim.x;
-    const int rw = hs / 4, pm = LINES_PLUS / 4;
+    // bins grow downward from the region tops: level l sits l + 1 words below
+    const int rw = hs / 4, dt = lay.dtop / 4, pt = lay.ptop / 4, mt = pt - LINES_MINUS / 4;
     for (int64_t b = U0 / Timg; b < batch && b * Timg < U1; ++b) {
         const int64_t a = max(U0, b * Timg) - b * Timg, e = min(U1, (b + 1) * Timg) - b * Timg;
         const int64_t wa = a + (e - a) * warp / NW, we = a + (e - a) * (warp + 1) / NW;
@@ -220,9 +225,9 @@ __global__ void __launch_bounds__(L2L_NTH, MINB) lines2d_kernel(const typename E
             if (r0 >= r1) continue;
             const int k0 = t * 62 - 1;
             if (k0 >= 1 && k0 + 63 <= g.W)
-                lines2d_item<DT, QM, VEC, false, PF, WS>(img, g, q, tt, g.v0 + r0, g.v0 + r1, k0, lane, sbw);
+                lines2d_item<DT, QM, VEC, false, PF, WS>(img, g, q, tt, topd, topp, g.v0 + r0, g.v0 + r1, k0, lane);
             else
-                lines2d_item<DT, QM, VEC, true, PF, WS>(img, g, q, tt, g.v0 + r0, g.v0 + r1, k0, lane, sbw);
+                lines2d_item<DT, QM, VEC, true, PF, WS>(img, g, q, tt, topd, topp, g.v0 + r0, g.v0 + r1, k0, lane);
         }
         __syncthreads();
         // fold: C = sum of signature rows, E = sum (4 - u) rows, EC = plus -
@@ -230,13 +235,13 @@ __global__ void __launch_bounds__(L2L_NTH, MINB) lines2d_kernel(const typename E
         unsigned long long* out = hist + b * 4 * M2;
         for (int l = threadIdx.x; l < M2; l += blockDim.x) {
             uint32_t c = 0, ed = 0;
-            int32_t ec = (int32_t)(hw[pm + l] - hw[pm + LINES_MINUS / 4 + l]);
-            hw[pm + l] = 0;
-            hw[pm + LINES_MINUS / 4 + l] = 0;
+            int32_t ec = (int32_t)(hw[pt - (l + 1)] - hw[mt - (l + 1)]);
+            hw[pt - (l + 1)] = 0;
+            hw[mt - (l + 1)] = 0;
 #pragma unroll
             for (int s = 0; s < L2L_SIG; ++s) {
-                const uint32_t v = hw[s * rw + l];
-                hw[s * rw + l] = 0;
+                const uint32_t v = hw[dt - s * rw - (l + 1)];
+                hw[dt - s * rw - (l + 1)] = 0;
                 c += v;
                 ed += (uint32_t)(4 - s % 5) * v;
                 ec -= (s / 5 - 1) * (int32_t)v;
@@ -252,13 +257,7 @@ __global__ void __launch_bounds__(L2L_NTH, MINB) lines2d_kernel(const typename E
 
 // 16-bit packed signature offsets: 14 hs + (M + 1) * 4 + base must fit
 static int lines2d_hs(int M) { return 255 * (int)cdiv(cdiv((int64_t)(M + 2) * 4, 255), 4) * 4; }
-static bool lines2d_ok(int M)
-{
-    const int hs = lines2d_hs(M);
-    const int sb = lines_sbase();
-    return (M + 2) * 4 <= hs && (L2L_SIG - 1) * hs + (M + 1) * 4 + sb < LINES_PLUS &&
-           (M + 1) * 4 + sb < LINES_MINUS && hs + (M + 2) * 4 <= LINES_MINUS;
-}
+static bool lines2d_ok(int M) { return lines_layout_ok(lines2d_hs(M), L2L_SIG, M); }
 
 template <int DT, int QM>
 static int launch_lines2d(const ft_window* win, int64_t H, int64_t W, int64_t v0, int64_t v1, const ft_quant* qa,
@@ -275,10 +274,9 @@ static int launch_lines2d(const ft_window* win, int64_t H, int64_t W, int64_t v0
     g.n_items = std::max<int64_t>(win->batch, 1);
     const bool vec = W % 2 == 0 && (g.n_items <= 1 || win->batch_stride % 2 == 0) &&
                      reinterpret_cast<uintptr_t>(win->data) % (2 * sizeof(T)) == 0;
-    if (const int rc = lines_check_sbase()) return rc;
     QuantDev qd = qdev(qa);
     if (QM == FT_Q_POW2) qd.inv = M > 0 ? qd.scale / (float)M : 0.f;
-    const size_t smem = (size_t)(LINES_PLUS + LINES_MINUS + g.hs);
+    const size_t smem = (size_t)lines_layout(g.hs, L2L_SIG, M).end;
     using K = void (*)(const T*, LGeo, QuantDev, unsigned long long*);
     const bool single = g.n_items == 1;
     K kern = single ? (vec ? lines2d_kernel<DT, QM, true, 8, 1, 0> : lines2d_kernel<DT, QM, false, 8, 1, 0>)

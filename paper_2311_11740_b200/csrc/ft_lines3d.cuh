@@ -62,21 +62,17 @@ constexpr int LINES_MINB = LINES_MINB_DEF;  // CTAs per SM the registers are bud
 constexpr int LINES_R = LINES_R_DEF;    // lattice rows per warp strip
 
 __host__ __device__ inline int lines_nsig(bool fold) { return fold ? 21 : 7; }
-// Shared layout: signature rows at 0 (at most 64 KB: the 16-bit packed row
-// offsets), the plus row at LINES_PLUS and the minus row LINES_MINUS above
-// it; both bases are constants, so every ATOMS address is [R + UR (+imm)].
-__host__ __device__ inline int lines_end(int hs, bool) { return LINES_PLUS + LINES_MINUS + hs; }
 
 // One warp strip (R lattice rows x 62 lattice columns) marching the planes of
-// a chunk [ia, ib).  Shared memory (lines_end): signature rows at 0, the
-// plus / minus rows of the EC events of the B/C/D lines (and of the A lines
-// unless FOLD) at LINES_PLUS / LINES_PLUS + LINES_MINUS.
+// a chunk [ia, ib).  Shared memory (lines_layout): the signature rows below
+// topd, the plus / minus rows of the EC events of the B/C/D lines (and of the
+// A lines unless FOLD) below topp (topd / topp: shared addresses).
 // EDGE 0: interior strip (no guards); 1: every row present, columns outside
 // the field (clamped loads, masked halves); 2: rows and columns guarded.
 template <int DT, int QM, bool VEC, int R, bool FOLD, int DS, int EDGE>
 __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restrict__ buf, const LGeo& g,
-                                           const QuantDev& q, const float* __restrict__ tt, char* __restrict__ h,
-                                           int64_t ia, int64_t ib, int j0, int k0, int lane, uint32_t sbw)
+                                           const QuantDev& q, const float* __restrict__ tt, uint32_t topd_u,
+                                           uint32_t topp_u, int64_t ia, int64_t ib, int j0, int k0, int lane)
 {
     using P2 = typename Pair<DT>::T;
     using T = typename Elem<DT>::T;
@@ -87,7 +83,8 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
     const int Di = DS > 0 ? DS : (int)g.D;
     const int64_t pe = g.W * (int64_t)Di;
     const uint32_t sent4 = (uint32_t)(g.M + 1) * 4u;
-    const uint32_t S2 = sent4 * 0x10001u + sbw;  // sentinel level word (with the shared base)
+    constexpr uint32_t sbw = LINES_REL0;         // packed words: (level + 1) * 4 per half
+    const uint32_t S2 = sent4 * 0x10001u + sbw;  // sentinel level word
     const uint32_t hk = (uint32_t)g.hk;  // signature row stride / 255
     const float Mf = (float)g.M;
     // lane l holds cells kk, kk+1 (kk even: aligned pair loads); lattice
@@ -98,7 +95,10 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
     // through a shuffle so that ptxas keeps a mask register (one 3-input LOP3)
     // instead of SEL on a predicate
     const uint32_t lmask = __shfl_sync(FULL, lane == 0 ? 0xFFFF0000u : lane == 31 ? 0x0000FFFFu : FULL, lane);
-    const uint32_t dummy2 = S2;    // sentinel bin (never read) of signature row 0 / the plus row
+    const uint32_t lsel = __shfl_sync(FULL, lane_sel(lane), lane);  // dense events: halo halves -> the dummy word
+    // the region tops as per-lane registers (through a shuffle: as uniform
+    // values ptxas re-materialises them with a move in front of every IDP)
+    const uint32_t topd = __shfl_sync(FULL, topd_u, lane), topp = __shfl_sync(FULL, topp_u, lane);
     const int n = (int)(ib - ia);
 
     // Absent cells (outside the field) read as the sentinel:
@@ -258,17 +258,17 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
                 // A line event iff both or neither i-neighbour is first; minus (max) iff t3
                 const uint32_t fA = ~(tmi ^ t3) & lmask;
                 const uint32_t aA = o.pV[r] | ((t3 << 8) & 0x80008000u);
-                sinc2<LINES_PLUS>(ev_sel(fA << 8, aA, dummy2));
+                sinc2(aA, ev_sel(fA << 8), topp);
             }
-            sinc2<0>(sel_mask(lmask, evS, dummy2));  // halo lanes: sentinel bin of row 0
+            sinc2(evS, lsel, topd);
             // B / C / D lines: event iff the along-i order flips at p-1; sign -1
             // (B, C): local min -> minus row; sign +1 (D): local max -> minus row
             const uint32_t B = vmin2(V[r - 1], W_);
             const uint32_t D = vmin2(C[r - 1], C[r]);
             const uint32_t nB = cmp2(o.pB[r], B), nC = cmp2(o.pC[r], C[r]), nD = cmp2(o.pD[r], D);
-            sinc2<LINES_PLUS>(ev_sel((o.eB[r] ^ nB) & lmask, o.pB[r] | (nB & 0x80008000u), dummy2));
-            sinc2<LINES_PLUS>(ev_sel((o.eC[r] ^ nC) & lmask, o.pC[r] | (nC & 0x80008000u), dummy2));
-            sinc2<LINES_PLUS>(ev_sel((o.eD[r] ^ nD) & lmask, o.pD[r] | (~nD & 0x80008000u), dummy2));
+            sinc2(o.pB[r] | (nB & 0x80008000u), ev_sel((o.eB[r] ^ nB) & lmask), topp);
+            sinc2(o.pC[r] | (nC & 0x80008000u), ev_sel((o.eC[r] ^ nC) & lmask), topp);
+            sinc2(o.pD[r] | (~nD & 0x80008000u), ev_sel((o.eD[r] ^ nD) & lmask), topp);
             x.pt3[r] = t3;
             tpj = t4;
             x.pWm[r] = Wm[r];
@@ -360,9 +360,9 @@ __global__ void __launch_bounds__(LINES_NTH, LINES_MINB) lines3d_kernel(const ty
     char* h = reinterpret_cast<char*>(smem_raw);
     const int M2 = g.M + 2;
     const int hs = g.hs;
-    const int end = lines_end(hs, FOLD);
-    float* tt = reinterpret_cast<float*>(h + LINES_PLUS + hs);  // threshold table: in the plus/minus gap
-    for (int i = threadIdx.x; i < end / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(h)[i] = 0;
+    const LLay lay = lines_layout(hs, lines_nsig(FOLD), g.M);
+    float* tt = reinterpret_cast<float*>(h + lay.tt);  // threshold table: in the minus/plus gap
+    for (int i = threadIdx.x; i < lay.end / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(h)[i] = 0;
     __syncthreads();  // the table lies inside the zeroed range
     if (QM != FT_Q_IDENTITY && QM != FT_Q_POW2)
         for (int i = threadIdx.x; i < M2; i += blockDim.x) tt[i] = q.tt[i];
@@ -370,17 +370,18 @@ __global__ void __launch_bounds__(LINES_NTH, LINES_MINB) lines3d_kernel(const ty
 
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x / 32;
-    const uint32_t sbw = lines_sb2(smem_raw);
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    const uint32_t topd = sb + (uint32_t)lay.dtop, topp = sb + (uint32_t)lay.ptop;
     if constexpr (MODE != 1) {
         // A: interior column tiles; B: the k-boundary ones (EDGE 1 march)
         const int64_t np = g.v1 - g.v0;
         const int ntk = g.tiles_k - g.kb_lo - g.kb_hi;
         cta_tiles<R>(g, ntk, np, warp, [&](int j0, int tk, int64_t ia, int64_t ib) {
-            lines_item<DT, QM, VEC, R, FOLD, DS, 0>(buf, g, q, tt, h, ia, ib, j0, (g.kb_lo + tk) * 62 - 1, lane, sbw);
+            lines_item<DT, QM, VEC, R, FOLD, DS, 0>(buf, g, q, tt, topd, topp, ia, ib, j0, (g.kb_lo + tk) * 62 - 1, lane);
         });
         cta_tiles<R>(g, g.kb_lo + g.kb_hi, np, warp, [&](int j0, int tk, int64_t ia, int64_t ib) {
             const int t = tk < g.kb_lo ? tk : g.tiles_k - g.kb_hi + (tk - g.kb_lo);
-            lines_item<DT, QM, VEC, R, FOLD, DS, 1>(buf, g, q, tt, h, ia, ib, j0, t * 62 - 1, lane, sbw);
+            lines_item<DT, QM, VEC, R, FOLD, DS, 1>(buf, g, q, tt, topd, topp, ia, ib, j0, t * 62 - 1, lane);
         });
     }
     if constexpr (MODE != 0) {
@@ -395,20 +396,21 @@ __global__ void __launch_bounds__(LINES_NTH, LINES_MINB) lines3d_kernel(const ty
             const int j0 = g.rf_j0[rem - tk * g.rf_n];
             const int64_t ia = g.v0 + ch * g.e_chunk;
             const int64_t ib = min(ia + (int64_t)g.e_chunk, g.v1);
-            lines_item<DT, QM, VEC, R, FOLD, DS, 2>(buf, g, q, tt, h, ia, ib, j0, tk * 62 - 1, lane, sbw);
+            lines_item<DT, QM, VEC, R, FOLD, DS, 2>(buf, g, q, tt, topd, topp, ia, ib, j0, tk * 62 - 1, lane);
         }
     }
     __syncthreads();
     // fold: C = sum of signature rows, F = sum (6 - u) rows, EC = A events (row
     // groups, or plus/minus when !FOLD) + plus - minus, X = EC - F + C
+    // (bins grow downward from the region tops: level l sits l + 1 words below)
     const uint32_t* hw = reinterpret_cast<const uint32_t*>(h);
-    const int rw = hs / 4, sb = 0, pm = LINES_PLUS / 4;
+    const int rw = hs / 4, dt = lay.dtop / 4, pt = lay.ptop / 4;
     for (int l = threadIdx.x; l < M2; l += blockDim.x) {
         uint32_t c = 0, f = 0;
-        int32_t ec = (int32_t)(hw[pm + l] - hw[pm + LINES_MINUS / 4 + l]);
+        int32_t ec = (int32_t)(hw[pt - (l + 1)] - hw[pt - LINES_MINUS / 4 - (l + 1)]);
 #pragma unroll
         for (int s = 0; s < lines_nsig(FOLD); ++s) {
-            const uint32_t v = hw[sb + s * rw + l];
+            const uint32_t v = hw[dt - s * rw - (l + 1)];
             c += v;
             f += (uint32_t)(6 - s % 7) * v;
             if (FOLD) ec += (s / 7 - 1) * (int32_t)v;
@@ -420,20 +422,12 @@ __global__ void __launch_bounds__(LINES_NTH, LINES_MINB) lines3d_kernel(const ty
     }
 }
 
-// 16-bit packed signature offsets: (rows - 1) * hs + level * 4 must fit
 // signature rows are 255 K bytes apart (K a multiple of 4: word-aligned rows)
 static int lines_hs(int M) { return 255 * (int)cdiv(cdiv((int64_t)(M + 2) * 4, 255), 4) * 4; }
-// 16-bit packed signature offsets: (rows - 1) * hs + level * 4 must fit
-static bool lines_fold_ok(int M, int hs)
-{
-    return 20 * hs + (M + 1) * 4 + lines_sbase() < LINES_PLUS && (M + 2) * 4 <= hs;
-}
-static bool lines_ok(int M)
-{
-    const int sb = lines_sbase();
-    return (M + 1) * 4 + sb < LINES_MINUS && 6 * lines_hs(M) + (M + 1) * 4 + sb < LINES_PLUS &&
-           lines_hs(M) + (M + 2) * 4 <= LINES_MINUS;
-}
+// 16-bit packed bin offsets (lines_layout_ok): 21 rows with the folded A-line
+// events, else 7 rows + the A events in the plus / minus rows
+static bool lines_fold_ok(int M, int hs) { return lines_layout_ok(hs, 21, M); }
+static bool lines_ok(int M) { return lines_layout_ok(lines_hs(M), 7, M); }
 
 
 // Interior and boundary items in one launch (MODE 2)
@@ -516,9 +510,8 @@ static int launch_lines3d(const ft_window* win, int64_t H, int64_t W, int64_t D,
     g.four = 4;
     const bool vec = D % 2 == 0 && reinterpret_cast<uintptr_t>(win->data) % (2 * sizeof(T)) == 0;
     const bool fold = lines_fold_ok(M, g.hs);
-    const size_t smem = (size_t)lines_end(g.hs, fold);
+    const size_t smem = (size_t)lines_layout(g.hs, lines_nsig(fold), M).end;
     g.tiles_k = (int)((D + 1) / 62 + 1);  // tile t: lattice columns 62 t - 1 .. 62 t + 60
-    if (const int rc = lines_check_sbase()) return rc;
     QuantDev qd = qdev(qa);
     if (QM == FT_Q_POW2) qd.inv = M > 0 ? qd.scale / (float)M : 0.f;
     if (fold)
