@@ -17,7 +17,7 @@
 #include <algorithm>
 
 #include "ft_common.cuh"
-#include "ft_lattice.cuh"
+#include "ft_lines.cuh"
 #include "ft_tables.h"
 
 namespace ft {
@@ -87,11 +87,13 @@ __device__ __forceinline__ void hm_cswap2(uint32_t& a, uint32_t& b)
     a = lo;
 }
 
-// BA (7 rows of byte offsets + the shared base fit 16 bits: M <= ~2260):
-// keys are level * 4 + slot + hb per half, hb = the histogram's shared address
-// (a multiple of 4: order and slot bits untouched), so a key with its slot
-// bits masked IS the shared address of the level's bin in row 0 -- no shift,
-// no index -> address arithmetic.  Otherwise 16-bit word indices.
+// BA (6 rows of byte offsets fit 16 bits: M <= ~2330): keys are level * 4 +
+// slot + 4 per half, so a key with its slot bits masked IS the offset
+// rel = (level + 1) * 4 of the level's bin BELOW the top of row 0; the
+// histogram grows downward from its top (row r another r * 4 (M + 2) lower,
+// the dummy word AT the top), and one IDP.2A per half (sinc2, ft_lines.cuh)
+// does the half split, the halo / range select and the address -- no shift,
+// no select, no index -> address arithmetic.  Otherwise 16-bit word indices.
 template <int DT, int QM, bool VEC, bool EDGE, bool BA>
 __device__ __forceinline__ void hm_item(const typename Elem<DT>::T* __restrict__ img, const Geo2& g,
                                         const QuantDev& q, const float* __restrict__ tt, uint32_t* __restrict__ h,
@@ -103,13 +105,15 @@ __device__ __forceinline__ void hm_item(const typename Elem<DT>::T* __restrict__
     const int Wi = (int)g.W;
     const uint32_t M2 = (uint32_t)g.M + 2u;
     const uint32_t sent4 = ((uint32_t)g.M + 1u) * 4u;
-    const uint32_t hbK = BA ? hb * K1 : 0u;
+    const uint32_t hbK = BA ? LINES_REL0 : 0u;  // BA keys: level * 4 + slot + 4
     const uint32_t S = sent4 * K1 + hbK;
     const int kk = k0 - 1 + 2 * lane;
     // vertex columns kk (low half) and kk+1 (high half) that this lane books
     const bool vlo = lane != 0 && kk >= 0 && kk <= Wi, vhi = lane != 31 && kk + 1 >= 0 && kk + 1 <= Wi;
     const uint32_t vmask = __shfl_sync(FULL, (vlo ? 0x0000FFFFu : 0u) | (vhi ? 0xFFFF0000u : 0u), lane);
-    const uint32_t dummy = BA ? (hb + 24u * M2) * K1 : 6u * M2 * K1;
+    const uint32_t vsel = __shfl_sync(FULL, (vlo ? 0x000000FFu : 0u) | (vhi ? 0xFF000000u : 0u), lane);  // sinc2 selector
+    const uint32_t top = __shfl_sync(FULL, hb + 24u * M2, lane);  // BA: the top of row 0 = the dummy word
+    const uint32_t dummy = 6u * M2 * K1;
     const bool okx = kk >= 0 && kk < Wi, oky = kk + 1 >= 0 && kk + 1 < Wi;
     const int kc = !EDGE ? kk : VEC ? min(max(kk, 0), Wi - 2) : min(max(kk, 0), Wi - 1);
     const int n = (int)(ib - ia);
@@ -143,11 +147,7 @@ __device__ __forceinline__ void hm_item(const typename Elem<DT>::T* __restrict__
             const uint32_t w[4] = {s0 & LM, (s1 & LM) + (K1 + diag) * Sb, (s2 & LM) + (3u * K1 + diag) * Sb,
                                    (s3 & LM) + 5u * Sb * K1};
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const uint32_t x = (w[e] & vmask) | (dummy & ~vmask);
-                ft_sh_inc(x & 0xFFFFu);
-                ft_sh_inc(x >> 16);
-            }
+            for (int e = 0; e < 4; ++e) sinc2(w[e], vsel, top);
         } else {
             const uint32_t i0 = (s0 >> 2) & 0x3FFF3FFFu;
             const uint32_t i1 = ((s1 >> 2) & 0x3FFF3FFFu) + (K1 + diag) * M2;
@@ -217,7 +217,6 @@ __global__ void __launch_bounds__(HM_NTH, 2) hist2d_march(const typename Elem<DT
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t hb = (uint32_t)__cvta_generic_to_shared(h);
-    if (BA && hb + 28u * (uint32_t)M2 > 0xFFFFu) __trap();  // the launcher leaves 2 KB for the base
     constexpr int NW = HM_NTH / 32;
     const int64_t nrows = g.v1 - g.v0;
     const int ntiles = g.tiles;
@@ -248,7 +247,8 @@ __global__ void __launch_bounds__(HM_NTH, 2) hist2d_march(const typename Elem<DT
         for (int i = threadIdx.x; i < 7 * M2; i += blockDim.x) {
             const uint32_t v = h[i];
             h[i] = 0;
-            if (v && i < 6 * M2) atomicAdd(&out[i], (unsigned long long)v);
+            // BA: bin (row r, level l) sits r M2 + l + 1 words below word 6 M2
+            if (v && i < 6 * M2) atomicAdd(&out[BA ? 6 * M2 - 1 - i : i], (unsigned long long)v);
         }
         __syncthreads();
     }
@@ -283,7 +283,7 @@ static int launch2(const ft_window* win, int64_t H, int64_t W, int64_t v0, int64
 #ifdef HM2_NO_BA
         const bool ba = false;
 #else
-        const bool ba = 28 * M2 + 2048 <= 0xFFFF;  // byte addresses in the 16-bit halves (M <= 2265)
+        const bool ba = 24 * M2 <= 0xFFFF;  // 6 rows of byte offsets in the 16-bit halves (M <= 2728)
 #endif
         auto kern = ba ? (vec ? hist2d_march<DT, QM, true, true> : hist2d_march<DT, QM, false, true>)
                        : (vec ? hist2d_march<DT, QM, true, false> : hist2d_march<DT, QM, false, false>);
