@@ -65,6 +65,13 @@ typedef struct ft_quant {
     float scale;
     float bias;
     const float *thresholds;
+    /* the (lo, hi) of quantize_with_range the table was built from; 0, 0 when
+     * unknown.  For uint8 / uint16 inputs and an integer range 0 <= lo < hi
+     * the line kernels then decode levels in exact integer arithmetic
+     * (floor((2 (x - lo) M + (hi - lo)) / (2 (hi - lo))) by a multiply-high,
+     * checked against the float64 formula for every input value when a range
+     * is first seen) instead of the table. */
+    double lo, hi;
 } ft_quant;
 
 /* A device-resident run of consecutive rows (2D) or planes (3D) of a field
@@ -238,11 +245,14 @@ int ft_bmp_decode(const uint8_t *raw, int64_t H, int64_t W, int64_t row_stride, 
                   void *stream);
 
 /* Verification hook (tests only, not a reference interface): run one of the
- * three device quantizers the fused kernels inline -- path 0 to_level (map /
- * wide kernels, ft_quantize), 1 to_level4 (march / lattice kernels, incl. the
+ * device quantizers the fused kernels inline -- path 0 to_level (map / wide
+ * kernels, ft_quantize), 1 to_level4 (march / lattice kernels, incl. the
  * table-free FT_Q_POW2 form), 2 pack_pow2_sat (line kernels, float32 pairs,
- * FT_Q_POW2 only, n even) -- over a flat float32 / uint16 buffer into int32
- * levels, so every input value can be checked against fields.py:20-33. */
+ * FT_Q_POW2 only, n even), 3 the line kernels' exact integer decoding of
+ * uint16 pairs (integer ranges lo < hi <= 65535 with q->lo / q->hi set, n
+ * even; FT_ERR_ARG for other ranges) -- over a flat float32 / uint16 buffer
+ * into int32 levels, so every input value can be checked against
+ * fields.py:20-33. */
 int ft_quantize_probe(const void *x, int32_t dtype, int64_t n, const ft_quant *q, int32_t M, int32_t path,
                       int32_t *out, void *stream);
 

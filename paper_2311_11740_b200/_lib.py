@@ -25,7 +25,8 @@ FT_KIND_MAP, FT_KIND_FUSED = 0, 1
 
 class ft_quant(ctypes.Structure):
     _fields_ = [("mode", ctypes.c_int32), ("negate", ctypes.c_int32), ("scale", ctypes.c_float),
-                ("bias", ctypes.c_float), ("thresholds", ctypes.c_void_p)]
+                ("bias", ctypes.c_float), ("thresholds", ctypes.c_void_p),
+                ("lo", ctypes.c_double), ("hi", ctypes.c_double)]
 
 
 class ft_window(ctypes.Structure):

@@ -86,7 +86,12 @@ struct QuantDev {
     float scale, bias;
     const float* tt; // device, M+2 entries (kernels stage a shared copy)
     float inv;       // FT_Q_POW2: 1 / hi (exact, a power of two), set per launch
+    // FT_Q_UMAGIC (internal: uint8 / uint16 inputs, integer range lo < hi):
+    // level = ((clamp(x, lo, hi) - lo) * u_mul + u_add) * u_magic >> (32 + u_shift)
+    uint32_t u_lo2, u_hi2;  // lo, hi in both 16-bit halves
+    uint32_t u_mul, u_add, u_magic, u_shift;
 };
+constexpr int FT_Q_UMAGIC = 4;  // internal quantizer mode, never in an ft_quant
 
 template <int DT, int QM>
 __device__ __forceinline__ uint32_t to_level(typename Elem<DT>::T raw, const float* __restrict__ tt,

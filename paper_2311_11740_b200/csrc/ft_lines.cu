@@ -14,7 +14,15 @@ __global__ void quant_probe_kernel(const typename Elem<DT>::T* __restrict__ x, i
                                    int32_t* __restrict__ out)
 {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    if constexpr (PATH == 2) {
+    if constexpr (PATH == 3) {
+        using P2 = typename Pair<DT>::T;
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; 2 * i < n; i += stride) {
+            const P2 v = reinterpret_cast<const P2*>(x)[i];
+            const uint32_t w = pack_pair_umagic<DT>(v, q, 4u, 0u);
+            out[2 * i] = (int32_t)((w & 0xFFFFu) >> 2);
+            out[2 * i + 1] = (int32_t)(w >> 18);
+        }
+    } else if constexpr (PATH == 2) {
         using P2 = typename Pair<DT>::T;
         const float Mf = (float)M;
         for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; 2 * i < n; i += stride) {
@@ -40,12 +48,22 @@ using namespace ft;
 extern "C" int ft_quantize_probe(const void* x, int32_t dtype, int64_t n, const ft_quant* q, int32_t M,
                                  int32_t path, int32_t* out, void* stream)
 {
-    if (!x || !q || !out || n < 0 || M < 1 || path < 0 || path > 2) return FT_ERR_ARG;
+    if (!x || !q || !out || n < 0 || M < 1 || path < 0 || path > 3) return FT_ERR_ARG;
     if (q->mode == FT_Q_IDENTITY || !q->thresholds || (dtype != FT_F32 && dtype != FT_U16)) return FT_ERR_ARG;
     const int qm = effective_qmode(q, path != 0);
     if (path == 2 && (dtype != FT_F32 || qm != FT_Q_POW2 || n % 2)) return FT_ERR_ARG;
     if (n == 0) return FT_OK;
     QuantDev qd = qdev(q);
+    if (path == 3) {
+        // the line kernels' integer decoding of uint16 pairs (FT_Q_UMAGIC); FT_ERR_ARG
+        // when the range does not qualify (they would take the table then)
+        if (dtype != FT_U16 || n % 2 || !umagic_fill(q, M, 65536, qd)) return FT_ERR_ARG;
+        const int g3 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n / 2, 256), 148 * 16));
+        quant_probe_kernel<FT_U16, FT_Q_UMAGIC, 3><<<g3, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+            static_cast<const uint16_t*>(x), n, qd, M, out);
+        FT_CUDA_TRY(cudaGetLastError());
+        return FT_OK;
+    }
     qd.mode = qm;
     if (qm == FT_Q_POW2) qd.inv = q->scale / (float)M;  // 1 / hi, as launch_lines3d sets it
     cudaStream_t st = static_cast<cudaStream_t>(stream);

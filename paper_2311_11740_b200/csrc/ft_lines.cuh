@@ -2,6 +2,10 @@
 // kernels (ft_lines.cu: 3D, ft_lines2d.cu: 2D): packed 16-bit bin offsets, the
 // FMA-pipe quantizer, the dummy-address shared increments, the shared layout.
 #pragma once
+#include <algorithm>
+#include <cmath>
+#include <mutex>
+
 #include "ft_lattice.cuh"
 
 namespace ft {
@@ -47,6 +51,63 @@ __device__ __forceinline__ uint32_t pack_pow2_sat(const typename Pair<DT>::T& v,
     asm("fma.rm.f32x2 %0, %1, %2, %3;" : "=l"(y) : "l"(ab), "l"(m2), "l"(0x3F0000003F000000ull));
     asm("add.rm.f32x2 %0, %1, %2;" : "=l"(z) : "l"(y), "l"(0x4B0000004B000000ull));
     return __byte_perm((uint32_t)z, (uint32_t)(z >> 32), 0x5410) * four + sb2;  // IMAD: FMA pipe
+}
+
+// FT_Q_UMAGIC: uint8 / uint16 pairs decoded in exact integer arithmetic.  For
+// integers x, lo < hi the reference level clip(floor((x - lo) M / (hi - lo) +
+// 0.5), 0, M) (fields.py:20-33) is floor((2 t M + R) / (2 R)) with t =
+// clamp(x, lo, hi) - lo and R = hi - lo: the numerator stays below 2^31 and
+// the division by 2 R is a multiply-high and a shift (Granlund-Montgomery),
+// all of it checked against the float64 formula for EVERY input value on the
+// host before a range is used (umagic_fill).  Two packed clamps, no
+// int<->float conversion (the quarter-rate XU pipe), no table load.
+template <int DT>
+__device__ __forceinline__ uint32_t pack_pair_umagic(const typename Pair<DT>::T& v, const QuantDev& q, uint32_t four,
+                                                     uint32_t rel0)
+{
+    const uint32_t w = __byte_perm((uint32_t)v.x, (uint32_t)v.y, 0x5410);
+    const uint32_t t2 = __vmaxu2(__vminu2(w, q.u_hi2), q.u_lo2) - q.u_lo2;
+    const uint32_t l0 = __umulhi((t2 & 0xFFFFu) * q.u_mul + q.u_add, q.u_magic) >> q.u_shift;
+    const uint32_t l1 = __umulhi((t2 >> 16) * q.u_mul + q.u_add, q.u_magic) >> q.u_shift;
+    return __byte_perm(l0, l1, 0x5410) * four + rel0;
+}
+
+// Host side of FT_Q_UMAGIC: true (and qd filled) iff the input type has nvals
+// = 256 / 65536 values, the range is an increasing integer one inside it and
+// the integer formula reproduces the float64 reference for every value.
+static inline bool umagic_fill(const ft_quant* qa, int M, int nvals, QuantDev& qd)
+{
+    if (!qa || qa->negate || M < 1 || !(qa->lo < qa->hi)) return false;
+    if (qa->mode != FT_Q_TABLE && qa->mode != FT_Q_TABLE_ROBUST && qa->mode != FT_Q_POW2) return false;
+    const double lo = qa->lo, hi = qa->hi;
+    if (lo < 0 || hi > nvals - 1 || lo != (double)(int64_t)lo || hi != (double)(int64_t)hi) return false;
+    const uint64_t L = (uint64_t)lo, R = (uint64_t)hi - L, mul = 2ull * (uint64_t)M, d = 2 * R;
+    if (R * mul + R >= (1ull << 31)) return false;
+    int lg = 0;
+    while ((1ull << lg) < d) ++lg;  // ceil(log2 d) >= 1
+    const uint64_t magic = ((1ull << (31 + lg)) + d - 1) / d;
+    if (magic >> 32) return false;
+    // one verified range is remembered (the usual case: one field, many launches)
+    static std::mutex mu;
+    static double c_lo = 0, c_hi = 0;
+    static int c_M = 0, c_n = 0;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!(c_lo == lo && c_hi == hi && c_M == M && c_n == nvals)) {
+        for (int x = 0; x < nvals; ++x) {
+            const uint64_t t = (uint64_t)std::min<int64_t>(std::max<int64_t>(x, (int64_t)L), (int64_t)(L + R)) - L;
+            const uint64_t lev = ((t * mul + R) * magic) >> (31 + lg);
+            const double ref = std::min(std::max(std::floor(((double)x - lo) * (double)M / (hi - lo) + 0.5), 0.0), (double)M);
+            if ((double)lev != ref) return false;
+        }
+        c_lo = lo; c_hi = hi; c_M = M; c_n = nvals;
+    }
+    qd.u_lo2 = (uint32_t)L * 0x10001u;
+    qd.u_hi2 = (uint32_t)(L + R) * 0x10001u;
+    qd.u_mul = (uint32_t)mul;
+    qd.u_add = (uint32_t)R;
+    qd.u_magic = (uint32_t)magic;
+    qd.u_shift = (uint32_t)(lg - 1);
+    return true;
 }
 
 // Shared-memory increments of both 16-bit halves of a packed word of bin

@@ -146,6 +146,8 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
             uint32_t v;
             if constexpr (QM == FT_Q_POW2)
                 v = pack_pow2_sat<DT>(src[r], q.inv, Mf, g.four, sbw);
+            else if constexpr (QM == FT_Q_UMAGIC)
+                v = pack_pair_umagic<DT>(src[r], q, g.four, sbw);
             else
                 v = pack_pair<DT, QM, 0>(src[r], true, true, tt, q, g.M, sent4) + sbw;
             V[r] = EDGE ? sel_mask(lanekeep, v, S2) : v;
@@ -163,6 +165,8 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
                 uint32_t v;
                 if constexpr (QM == FT_Q_POW2)
                     v = pack_pow2_sat<DT>(src[r], q.inv, Mf, g.four, sbw);
+                else if constexpr (QM == FT_Q_UMAGIC)
+                    v = pack_pair_umagic<DT>(src[r], q, g.four, sbw);
                 else
                     v = pack_pair<DT, QM, 0>(src[r], true, true, tt, q, g.M, sent4) + sbw;
                 V[r] = EDGE ? sel_mask(lanekeep, v, S2) : v;
@@ -364,7 +368,7 @@ __global__ void __launch_bounds__(LINES_NTH, LINES_MINB) lines3d_kernel(const ty
     float* tt = reinterpret_cast<float*>(h + lay.tt);  // threshold table: in the minus/plus gap
     for (int i = threadIdx.x; i < lay.end / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(h)[i] = 0;
     __syncthreads();  // the table lies inside the zeroed range
-    if (QM != FT_Q_IDENTITY && QM != FT_Q_POW2)
+    if (QM != FT_Q_IDENTITY && QM != FT_Q_POW2 && QM != FT_Q_UMAGIC)
         for (int i = threadIdx.x; i < M2; i += blockDim.x) tt[i] = q.tt[i];
     __syncthreads();
 
@@ -485,7 +489,8 @@ static int launch_lines_pair(const ft_window* win, const LGeo& g, const QuantDev
 {
     // specialised on the common row lengths of the BASELINE configs' f32 / u16
     // fields (C4a / C5 f32, C4b u16); other inputs take the generic loop
-    constexpr bool spec = VEC && (DT == FT_F32 || DT == FT_U16) && QM != FT_Q_TABLE_ROBUST;
+    constexpr bool spec = VEC && (DT == FT_F32 || DT == FT_U16) && QM != FT_Q_TABLE_ROBUST &&
+                          !(DT == FT_U16 && QM == FT_Q_TABLE);  // u16 integer ranges run as FT_Q_UMAGIC
     if constexpr (spec) {
         switch (g.D) {
         case 2048: return launch_lines_two<DT, QM, VEC, FOLD, 2048>(win, g, qd, smem, hist, st);
@@ -514,6 +519,7 @@ static int launch_lines3d(const ft_window* win, int64_t H, int64_t W, int64_t D,
     g.tiles_k = (int)((D + 1) / 62 + 1);  // tile t: lattice columns 62 t - 1 .. 62 t + 60
     QuantDev qd = qdev(qa);
     if (QM == FT_Q_POW2) qd.inv = M > 0 ? qd.scale / (float)M : 0.f;
+    if (QM == FT_Q_UMAGIC && !umagic_fill(qa, M, DT == FT_U8 ? 256 : 65536, qd)) return FT_ERR_INTERNAL;
     if (fold)
         return vec ? launch_lines_pair<DT, QM, true, true>(win, g, qd, smem, hist, st)
                    : launch_lines_pair<DT, QM, false, true>(win, g, qd, smem, hist, st);

@@ -178,4 +178,5 @@ def device_struct(spec, device, f64=False):
     if t is None:
         t = torch.from_numpy(spec.table(f64)).to(device)
         _dev_tables[key] = t
-    return _lib.ft_quant(spec.mode, spec.negate, spec.scale, spec.bias, ctypes.c_void_p(t.data_ptr())), t
+    return _lib.ft_quant(spec.mode, spec.negate, spec.scale, spec.bias, ctypes.c_void_p(t.data_ptr()),
+                         float(spec.lo), float(spec.hi)), t

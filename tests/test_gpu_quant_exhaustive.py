@@ -114,3 +114,24 @@ def test_u16_every_value(ft, lo, hi, M):
     ref = _reference(x.to(torch.float32), lo, hi, M)
     for p in (0, 1):
         assert torch.equal(_probe(x, spec, M, p), ref), (lo, hi, M, p)
+    # path 3: the line kernels' exact integer decoding of uint16 pairs, taken
+    # for increasing integer ranges inside the type; other ranges are refused
+    # there (the kernels keep the table for them)
+    if lo < hi <= 65535:
+        assert torch.equal(_probe(x, spec, M, 3), ref), (lo, hi, M, 3)
+    else:
+        with pytest.raises(ValueError):
+            _probe(x, spec, M, 3)
+
+
+@pytest.mark.parametrize("lo,hi,M", [(0, 1, 1), (5, 6, 3), (12, 4000, 1023), (1000, 1001, 4095), (0, 65535, 16383),
+                                     (1, 65534, 2047), (0, 255, 255), (3, 250, 100), (32768, 32769, 7),
+                                     (0, 65535, 1), (17, 40001, 1000)])
+def test_u16_integer_decoding_every_value(ft, lo, hi, M):
+    """FT_Q_UMAGIC on all 65536 uint16 values for narrow, wide, odd and
+    extreme integer ranges against the float64 formula (fields.py:20-33)."""
+    import torch
+    x = torch.arange(65536, dtype=torch.int32, device="cuda").to(torch.uint16)
+    spec = ft.quant.QuantSpec.for_range(float(lo), float(hi), M)
+    ref = _reference(x.to(torch.float32), float(lo), float(hi), M)
+    assert torch.equal(_probe(x, spec, M, 3), ref), (lo, hi, M)
