@@ -31,6 +31,12 @@ namespace ft {
 constexpr int L2L_NTH = 512;  // 16 warps, each a 62-column strip
 // rows per (row block, column tile) piece (measured 64 / 96 / 128 / 256:
 // profiles/r02/s3/ab_lines2d_rb.log)
+#ifndef L2B_PF
+#define L2B_PF 6
+#endif
+#ifndef L2B_MINB
+#define L2B_MINB 2
+#endif
 constexpr int L2L_RB = 96;
 constexpr int L2L_SIG = 15;        // signature rows u + 5 (s + 1)
 
@@ -180,7 +186,7 @@ __device__ __forceinline__ void lines2d_item(const typename Elem<DT>::T* __restr
 // hist[image] (one __syncthreads pair per image).
 // PF / MINB: rows in flight per lane / CTAs per SM the registers are
 // budgeted for -- 8 / 1 for single images (latency-bound: more bytes in
-// flight per warp), 4 / 2 for batches (measured, profiles/r01/lines2d_notes.md).
+// flight per warp), 6 / 2 for batches (measured: profiles/r01/lines2d_notes.md, profiles/r02/s5/NOTES.md).
 template <int DT, int QM, bool VEC, int PF, int MINB, int WS>
 __global__ void __launch_bounds__(L2L_NTH, MINB) lines2d_kernel(const typename Elem<DT>::T* __restrict__ buf, LGeo g,
                                                              QuantDev q, unsigned long long* __restrict__ hist)
@@ -280,12 +286,12 @@ static int launch_lines2d(const ft_window* win, int64_t H, int64_t W, int64_t v0
     using K = void (*)(const T*, LGeo, QuantDev, unsigned long long*);
     const bool single = g.n_items == 1;
     K kern = single ? (vec ? lines2d_kernel<DT, QM, true, 8, 1, 0> : lines2d_kernel<DT, QM, false, 8, 1, 0>)
-                    : (vec ? lines2d_kernel<DT, QM, true, 4, 2, 0> : lines2d_kernel<DT, QM, false, 4, 2, 0>);
+                    : (vec ? lines2d_kernel<DT, QM, true, L2B_PF, L2B_MINB, 0> : lines2d_kernel<DT, QM, false, L2B_PF, L2B_MINB, 0>);
     // the BASELINE configs' row lengths (C2: 8192 f32 pow2, C3: 1024 u8
     // identity) with immediate-offset row loads
     if constexpr ((DT == FT_F32 && QM == FT_Q_POW2) || (DT == FT_U8 && QM == FT_Q_IDENTITY)) {
-        if (vec && W == 8192) kern = single ? lines2d_kernel<DT, QM, true, 8, 1, 8192> : lines2d_kernel<DT, QM, true, 4, 2, 8192>;
-        if (vec && W == 1024) kern = single ? lines2d_kernel<DT, QM, true, 8, 1, 1024> : lines2d_kernel<DT, QM, true, 4, 2, 1024>;
+        if (vec && W == 8192) kern = single ? lines2d_kernel<DT, QM, true, 8, 1, 8192> : lines2d_kernel<DT, QM, true, L2B_PF, L2B_MINB, 8192>;
+        if (vec && W == 1024) kern = single ? lines2d_kernel<DT, QM, true, 8, 1, 1024> : lines2d_kernel<DT, QM, true, L2B_PF, L2B_MINB, 1024>;
     }
     FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
