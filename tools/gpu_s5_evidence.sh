@@ -1,8 +1,8 @@
 #!/bin/bash
 # Session-5 evidence: GPU suite, smoke, bench + reference arm, ncu launch list of the bench,
 # event timings of every config, ncu --set full of every shipping hot kernel (summaries + SASS mix).
-mkdir -p gpurun_out/s5f /tmp/ncu
-O=gpurun_out/s5f
+mkdir -p gpurun_out/s5g /tmp/ncu
+O=gpurun_out/s5g
 nvidia-smi > $O/nvsmi.txt 2>&1
 timeout 2400 python -m pytest tests -m gpu -q --durations=10 > $O/pytest_gpu_all.log 2>&1; echo "rc=$?" >> $O/pytest_gpu_all.log
 timeout 300 python __graft_entry__.py > $O/smoke.log 2>&1; echo "rc=$?" >> $O/smoke.log
