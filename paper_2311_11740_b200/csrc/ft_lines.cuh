@@ -76,6 +76,24 @@ __device__ __forceinline__ uint32_t pack_pair_umagic(const typename Pair<DT>::T&
     return l1 * (four << 16) + (l0 * four + rel0);  // two IMADs (FMA pipe) instead of a PRMT + IMAD
 }
 
+// Identity levels of uint8 / uint16 pairs (C3: u8 images), packed: the pair as
+// two 16-bit halves (u8: one PRMT; u16: the loaded word), one packed min with
+// the sentinel M + 1 (the scalar path's clamp, ft_common.cuh to_level) and one
+// IMAD -- instead of a convert / min / shift per cell and a PRMT.
+template <int DT>
+__device__ __forceinline__ uint32_t pack_pair_ident(const typename Pair<DT>::T& v, uint32_t sent_lv2, uint32_t four,
+                                                    uint32_t rel0)
+{
+    uint32_t w;
+    if constexpr (DT == FT_U16) {
+        w = *reinterpret_cast<const uint32_t*>(&v);
+    } else {
+        static_assert(DT == FT_U8, "packed identity levels: uint8 / uint16 only");
+        w = __byte_perm((uint32_t)*reinterpret_cast<const uint16_t*>(&v), 0u, 0x4140);
+    }
+    return __vminu2(w, sent_lv2) * four + rel0;
+}
+
 // Host side of FT_Q_UMAGIC: true (and qd filled) iff the input type has nvals
 // = 256 / 65536 values, the range is an increasing integer one inside it and
 // the integer formula reproduces the float64 reference for every value.

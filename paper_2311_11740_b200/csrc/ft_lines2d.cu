@@ -60,6 +60,7 @@ __device__ __forceinline__ void lines2d_item(const typename Elem<DT>::T* __restr
     const uint32_t sent4 = (uint32_t)(g.M + 1) * 4u;
     constexpr uint32_t sbw = LINES_REL0;  // packed words: (level + 1) * 4 per half
     const uint32_t S2 = sent4 * 0x10001u + sbw;
+    const uint32_t sent_lv2 = (uint32_t)(g.M + 1) * 0x10001u;
     const uint32_t hk = (uint32_t)g.hk;
     const float Mf = (float)g.M;
     const int kk = k0 - 1 + 2 * lane;
@@ -85,6 +86,8 @@ __device__ __forceinline__ void lines2d_item(const typename Elem<DT>::T* __restr
         uint32_t v;
         if constexpr (QM == FT_Q_POW2)
             v = pack_pow2_sat<DT>(src, q.inv, Mf, g.four, sbw);
+        else if constexpr (QM == FT_Q_IDENTITY && (DT == FT_U8 || DT == FT_U16))
+            v = pack_pair_ident<DT>(src, sent_lv2, g.four, sbw);
         else
             v = pack_pair<DT, QM, 0>(src, true, true, tt, q, g.M, sent4) + sbw;
         return EDGE ? sel_mask(lanekeep, v, S2) : v;

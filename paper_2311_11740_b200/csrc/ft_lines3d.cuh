@@ -85,6 +85,7 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
     const uint32_t sent4 = (uint32_t)(g.M + 1) * 4u;
     constexpr uint32_t sbw = LINES_REL0;         // packed words: (level + 1) * 4 per half
     const uint32_t S2 = sent4 * 0x10001u + sbw;  // sentinel level word
+    const uint32_t sent_lv2 = (uint32_t)(g.M + 1) * 0x10001u;
     const uint32_t hk = (uint32_t)g.hk;  // signature row stride / 255
     const float Mf = (float)g.M;
     // lane l holds cells kk, kk+1 (kk even: aligned pair loads); lattice
@@ -148,6 +149,8 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
                 v = pack_pow2_sat<DT>(src[r], q.inv, Mf, g.four, sbw);
             else if constexpr (QM == FT_Q_UMAGIC)
                 v = pack_pair_umagic<DT>(src[r], q, g.four, sbw);
+            else if constexpr (QM == FT_Q_IDENTITY && (DT == FT_U8 || DT == FT_U16))
+                v = pack_pair_ident<DT>(src[r], sent_lv2, g.four, sbw);
             else
                 v = pack_pair<DT, QM, 0>(src[r], true, true, tt, q, g.M, sent4) + sbw;
             V[r] = EDGE ? sel_mask(lanekeep, v, S2) : v;
@@ -167,6 +170,8 @@ __device__ __forceinline__ void lines_item(const typename Elem<DT>::T* __restric
                     v = pack_pow2_sat<DT>(src[r], q.inv, Mf, g.four, sbw);
                 else if constexpr (QM == FT_Q_UMAGIC)
                     v = pack_pair_umagic<DT>(src[r], q, g.four, sbw);
+                else if constexpr (QM == FT_Q_IDENTITY && (DT == FT_U8 || DT == FT_U16))
+                    v = pack_pair_ident<DT>(src[r], sent_lv2, g.four, sbw);
                 else
                     v = pack_pair<DT, QM, 0>(src[r], true, true, tt, q, g.M, sent4) + sbw;
                 V[r] = EDGE ? sel_mask(lanekeep, v, S2) : v;
