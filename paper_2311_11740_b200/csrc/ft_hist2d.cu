@@ -127,7 +127,10 @@ __device__ __forceinline__ void hm_item(const typename Elem<DT>::T* __restrict__
         if (t >= t_lo && t < tf) dst = load_pair<DT, VEC>(at, true, EDGE ? kk + 1 < Wi : true);
     };
     auto quant_in = [&](const P2& src) -> uint32_t {
-        return pack_pair<DT, QM, 0>(src, !EDGE || okx, !EDGE || oky, tt, q, g.M, sent4) + hbK;
+        if constexpr (!EDGE && QM == FT_Q_IDENTITY && (DT == FT_U8 || DT == FT_U16))
+            return pack_pair_ident<DT>(src, (sent4 >> 2) * K1, 4u, hbK);  // packed clamp + one multiply-add
+        else
+            return pack_pair<DT, QM, 0>(src, !EDGE || okx, !EDGE || oky, tt, q, g.M, sent4) + hbK;
     };
     // one vertex row: sorted NW / NE keys of the row above in a, c
     uint32_t a, c;

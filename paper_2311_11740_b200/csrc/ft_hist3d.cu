@@ -22,7 +22,7 @@
 #include <algorithm>
 
 #include "ft_common.cuh"
-#include "ft_lattice.cuh"
+#include "ft_lines.cuh"
 #include "ft_tables.h"
 
 namespace ft {
@@ -248,7 +248,11 @@ __device__ __forceinline__ void hm3_item(const typename Elem<DT>::T* __restrict_
         const bool exists = t >= t_lo && t < t_hi;
 #pragma unroll
         for (int c = 0; c < NR; ++c) {
-            uint32_t v = pack_pair<DT, QM, 1>(src[c], !EDGE || okx, !EDGE || oky, tt, q, g.M, sent8) + bk.hb2;
+            uint32_t v;
+            if constexpr (!EDGE && QM == FT_Q_IDENTITY && (DT == FT_U8 || DT == FT_U16))
+                v = pack_pair_ident<DT>(src[c], (sent8 >> 3) * K1, 8u, bk.hb2);  // packed clamp + one multiply-add
+            else
+                v = pack_pair<DT, QM, 1>(src[c], !EDGE || okx, !EDGE || oky, tt, q, g.M, sent8) + bk.hb2;
             if (EDGE && !((rowok >> c) & 1u)) v = S;
             V[c] = exists ? v : S;
             Wm[c] = shift_pair(__shfl_up_sync(FULL, V[c], 1), V[c]);
