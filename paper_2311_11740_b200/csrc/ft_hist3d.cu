@@ -8,14 +8,17 @@
 // the transition class (type_n -> type_{n+1}, 40 classes)
 // instead of the reference's 15 q_in/q_out increments.  The classes of ranks
 // 1-3 are a function of the first four sorted slots and those of ranks 4-6 of
-// the last four, so two 4096-entry tables (one lookup each) classify all six
-// middle ranks.
+// the last four -- and, the pair classes only seeing XORs of slots, of those
+// slots RELATIVE to the first / last one: two 512-entry tables (one lookup
+// each) classify all six middle ranks; the march kernel keeps a copy per lane
+// (or per 4 lanes) in shared memory, the wide kernel reads the 4096-entry
+// absolute form from global memory.
 //
 // Two kernels:
 // * hist3d_march (default): a warp marches a strip of vertex rows along i
 //   (the slab axis) on packed 16-bit keys, two vertices per word, into a
-//   per-CTA shared-memory histogram -- M + 1 <= 8190 and the 40 x (M+2)
-//   histogram + tables in shared memory (M <= ~1150);
+//   per-CTA shared-memory histogram -- the 41 x (M+2) histogram + tables in
+//   shared memory (M <= ~1380);
 // * hist3d_wide (any M the reference accepts, e.g. u16 identity levels):
 //   one vertex per thread, 32-bit keys, events booked straight into the
 //   global u64 histogram.
@@ -74,24 +77,18 @@ __host__ __device__ __forceinline__ uint32_t slot_index(uint32_t a, uint32_t b, 
     return ((a & 7u) << 9) | ((b & 7u) << 6) | ((c & 7u) << 3) | (d & 7u);
 }
 
-// XT: lane-replicated XOR-relative tables (32 x NXT words each); otherwise the
-// two NTAB-entry absolute tables.
-template <bool XT>
+// The XOR-relative rank tables, RP copies each (lane l reads copy l % RP:
+// entry e at word RP e + l % RP).  RP = 32: one bank per lane, conflict-free;
+// RP = 8 (32 KB for both tables) when the histogram leaves no room for more.
+template <int RP>
 __device__ __forceinline__ void init_shared3(uint32_t* h, uint32_t* ta, uint32_t* tb, float* tt,
                                              const RankTables* __restrict__ rt, const QuantDev& q, int M2,
                                              bool table)
 {
     for (int i = threadIdx.x; i < NROW3 * M2; i += blockDim.x) h[i] = 0;
-    if constexpr (XT) {
-        for (int i = threadIdx.x; i < NXT * 32; i += blockDim.x) {
-            ta[i] = rt->xa[i >> 5];
-            tb[i] = rt->xb[i >> 5];
-        }
-    } else {
-        for (int i = threadIdx.x; i < NTAB; i += blockDim.x) {
-            ta[i] = rt->a[i];
-            tb[i] = rt->b[i];
-        }
+    for (int i = threadIdx.x; i < NXT * RP; i += blockDim.x) {
+        ta[i] = rt->xa[i / RP];
+        tb[i] = rt->xb[i / RP];
     }
     if (table)
         for (int i = threadIdx.x; i < M2; i += blockDim.x) tt[i] = q.tt[i];
@@ -153,7 +150,7 @@ constexpr int HM3_NTH = 512;    // 16 warps: 64 vertex rows per CTA tile
 struct Book3 {
     uint32_t hb2;      // 2 x shared address of the histogram in both halves: carried by every key
     uint32_t r39;      // 39 S: row 39 is the fixed class of rank 7
-    uint32_t ta, tb;   // shared addresses of the rank tables (XT: + 4 lane)
+    uint32_t ta, tb;   // shared addresses of the lane's copy of the rank tables
     uint32_t S, S16;   // row stride in bytes, 4 (M + 2) (< 2^16), and S << 16
     uint32_t c8;       // 8 as a run-time value: x * c8 + y stays an IMAD
 };
@@ -164,21 +161,16 @@ struct Book3 {
 // shared address, a multiple of 4, so order and slot bits are untouched):
 // with the slot bits cleared the high half's kc >> 17 -- and the low half's
 // (kc << 16) >> 17 -- IS the shared address of the level's bin in row 0.
-template <bool XT>
+template <int RP>
 __device__ __forceinline__ void book3_pair(const Book3& x, const uint32_t (&k)[8], bool lo, bool hi)
 {
     constexpr uint32_t S7 = 0x00070007u, LV = 0xFFF8FFF8u;
-    constexpr int SX = XT ? 9 : 14;  // index in the high half -> table byte offset (XT: * 128, else * 4)
-    uint32_t pa, pb;
-    if constexpr (XT) {
-        const uint32_t a1 = (k[1] ^ k[0]) & S7, a2 = (k[2] ^ k[0]) & S7, a3 = (k[3] ^ k[0]) & S7;
-        const uint32_t b1 = (k[6] ^ k[7]) & S7, b2 = (k[5] ^ k[7]) & S7, b3 = (k[4] ^ k[7]) & S7;
-        pa = (a1 * x.c8 + a2) * x.c8 + a3;  // 9 bits per half
-        pb = (b1 * x.c8 + b2) * x.c8 + b3;
-    } else {
-        pa = (((k[0] & S7) * x.c8 + (k[1] & S7)) * x.c8 + (k[2] & S7)) * x.c8 + (k[3] & S7);  // 12 bits per half
-        pb = (((k[4] & S7) * x.c8 + (k[5] & S7)) * x.c8 + (k[6] & S7)) * x.c8 + (k[7] & S7);
-    }
+    constexpr int SX = RP == 32 ? 9 : 11;  // index in the high half -> table byte offset (* 4 RP)
+    // slot indices relative to the first (ranks 1-3) / last (ranks 4-6) sorted slot, 9 bits per half
+    const uint32_t a1 = (k[1] ^ k[0]) & S7, a2 = (k[2] ^ k[0]) & S7, a3 = (k[3] ^ k[0]) & S7;
+    const uint32_t b1 = (k[6] ^ k[7]) & S7, b2 = (k[5] ^ k[7]) & S7, b3 = (k[4] ^ k[7]) & S7;
+    const uint32_t pa = (a1 * x.c8 + a2) * x.c8 + a3;
+    const uint32_t pb = (b1 * x.c8 + b2) * x.c8 + b3;
     uint32_t kc[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) kc[e] = k[e] & LV;
@@ -203,7 +195,7 @@ __device__ __forceinline__ void book3_pair(const Book3& x, const uint32_t (&k)[8
     if (hi) book(ft_sh_ld((pa >> SX) + x.ta), ft_sh_ld((pb >> SX) + x.tb), kc);
 }
 
-template <int DT, int QM, bool VEC, bool EDGE, bool XT>
+template <int DT, int QM, bool VEC, bool EDGE, int RP>
 __device__ __forceinline__ void hm3_item(const typename Elem<DT>::T* __restrict__ buf, const Geo3& g,
                                          const QuantDev& q, const float* __restrict__ tt, const Book3& bk,
                                          int64_t ia, int64_t ib, int j0, int k0, int lane)
@@ -288,7 +280,7 @@ __device__ __forceinline__ void hm3_item(const typename Elem<DT>::T* __restrict_
             keys4(V, Wm, v, 1u, u);
             uint32_t k8[8] = {prev[v][0], prev[v][1], prev[v][2], prev[v][3], u[0], u[1], u[2], u[3]};
             merge44x2(k8);
-            book3_pair<XT>(bk, k8, vrow[v] && clo, vrow[v] && chi);
+            book3_pair<RP>(bk, k8, vrow[v] && clo, vrow[v] && chi);
 #pragma unroll
             for (int e = 0; e < 4; ++e) prev[v][e] = u[e] - K1;
         }
@@ -306,7 +298,7 @@ __device__ __forceinline__ void hm3_item(const typename Elem<DT>::T* __restrict_
     }
 }
 
-template <int DT, int QM, bool VEC, bool XT>
+template <int DT, int QM, bool VEC, int RP>
 __global__ void __launch_bounds__(HM3_NTH, 1) hist3d_march(const typename Elem<DT>::T* __restrict__ buf, Geo3 g,
                                                           QuantDev q, const RankTables* __restrict__ rt,
                                                           unsigned long long* __restrict__ hist)
@@ -315,9 +307,9 @@ __global__ void __launch_bounds__(HM3_NTH, 1) hist3d_march(const typename Elem<D
     const int M2 = g.M + 2;
     uint32_t* h = reinterpret_cast<uint32_t*>(smem_raw);
     uint32_t* ta = h + NROW3 * M2;
-    uint32_t* tb = ta + (XT ? NXT * 32 : NTAB);
-    float* tt = reinterpret_cast<float*>(tb + (XT ? NXT * 32 : NTAB));
-    init_shared3<XT>(h, ta, tb, tt, rt, q, M2, QM != FT_Q_IDENTITY && QM != FT_Q_POW2);
+    uint32_t* tb = ta + NXT * RP;
+    float* tt = reinterpret_cast<float*>(tb + NXT * RP);
+    init_shared3<RP>(h, ta, tb, tt, rt, q, M2, QM != FT_Q_IDENTITY && QM != FT_Q_POW2);
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     Book3 bk;
@@ -329,8 +321,8 @@ __global__ void __launch_bounds__(HM3_NTH, 1) hist3d_march(const typename Elem<D
     bk.S = 4u * (uint32_t)M2;
     bk.S16 = bk.S << 16;
     bk.r39 = 39u * bk.S;
-    bk.ta = (uint32_t)__cvta_generic_to_shared(ta) + (XT ? 4u * lane : 0u);
-    bk.tb = (uint32_t)__cvta_generic_to_shared(tb) + (XT ? 4u * lane : 0u);
+    bk.ta = (uint32_t)__cvta_generic_to_shared(ta) + 4u * (lane % RP);
+    bk.tb = (uint32_t)__cvta_generic_to_shared(tb) + 4u * (lane % RP);
     bk.c8 = g.c8;
     constexpr int TJ = (HM3_NTH / 32) * HMR;
     const int64_t np = g.v1 - g.v0;
@@ -347,9 +339,9 @@ __global__ void __launch_bounds__(HM3_NTH, 1) hist3d_march(const typename Elem<D
         if (j0 > g.W) continue;
         const int64_t ia = g.v0 + p;
         if (j0 >= 1 && j0 + HMR <= g.W && k0 >= 1 && k0 + 63 <= g.D)
-            hm3_item<DT, QM, VEC, false, XT>(buf, g, q, tt, bk, ia, ia + len, j0, k0, lane);
+            hm3_item<DT, QM, VEC, false, RP>(buf, g, q, tt, bk, ia, ia + len, j0, k0, lane);
         else
-            hm3_item<DT, QM, VEC, true, XT>(buf, g, q, tt, bk, ia, ia + len, j0, k0, lane);
+            hm3_item<DT, QM, VEC, true, RP>(buf, g, q, tt, bk, ia, ia + len, j0, k0, lane);
     }
     __syncthreads();
     flush_hist(h, hist, M2);
@@ -472,15 +464,11 @@ static const RankTables* device_rank_tables()
     return dev_tabs[dev];
 }
 
-// shared bytes of hist3d_march: the 40 x (M+2) histogram, both rank tables, the threshold table
-static size_t march3_smem(int M, bool xt) { return (size_t)(NROW3 * (M + 2) + 2 * (xt ? NXT * 32 : NTAB) + (M + 2)) * 4; }
-static bool march3_ok(int M) { return M + 1 <= 4095 && march3_smem(M, false) <= 227 * 1024; }
-// the lane-replicated tables (128 KB) beside the histogram: M <= ~600
-#ifdef HM3_FORCE_NOXT
-static bool march3_xt(int) { return false; }
-#else
-static bool march3_xt(int M) { return march3_smem(M, true) <= 227 * 1024; }
-#endif
+// shared bytes of hist3d_march: the 41 x (M+2) histogram, RP copies of both rank tables, the threshold table
+static size_t march3_smem(int M, int rp) { return (size_t)(NROW3 * (M + 2) + 2 * NXT * rp + (M + 2)) * 4; }
+static bool march3_ok(int M) { return M + 1 <= 4095 && march3_smem(M, 8) <= 227 * 1024; }
+// one table copy per lane (128 KB) beside the histogram: M <= 601
+static bool march3_rp32(int M) { return march3_smem(M, 32) <= 227 * 1024; }
 
 template <int DT, int QM>
 static int launch3(const ft_window* win, int64_t H, int64_t W, int64_t D, int64_t v0, int64_t v1,
@@ -498,11 +486,11 @@ static int launch3(const ft_window* win, int64_t H, int64_t W, int64_t D, int64_
     const int nsm = sm_count();
     if (march3_ok(M)) {
         // register march: every vertex (j, k) in [0, W] x [0, D]
-        const bool xt = march3_xt(M);
-        const size_t sm = march3_smem(M, xt);
+        const bool wide = march3_rp32(M);
+        const size_t sm = march3_smem(M, wide ? 32 : 8);
         const bool vec = D % 2 == 0 && reinterpret_cast<uintptr_t>(buf) % (2 * sizeof(T)) == 0;
-        auto kern = xt ? (vec ? hist3d_march<DT, QM, true, true> : hist3d_march<DT, QM, false, true>)
-                       : (vec ? hist3d_march<DT, QM, true, false> : hist3d_march<DT, QM, false, false>);
+        auto kern = wide ? (vec ? hist3d_march<DT, QM, true, 32> : hist3d_march<DT, QM, false, 32>)
+                         : (vec ? hist3d_march<DT, QM, true, 8> : hist3d_march<DT, QM, false, 8>);
         g.c8 = 8;
         FT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         int per_sm = 0;
