@@ -241,9 +241,16 @@ __device__ __forceinline__ void hm3_item(const typename Elem<DT>::T* __restrict_
 #pragma unroll
         for (int c = 0; c < NR; ++c) {
             uint32_t v;
-            if constexpr (!EDGE && QM == FT_Q_IDENTITY && (DT == FT_U8 || DT == FT_U16))
+            if constexpr (!EDGE && QM == FT_Q_IDENTITY && (DT == FT_U8 || DT == FT_U16)) {
                 v = pack_pair_ident<DT>(src[c], (sent8 >> 3) * K1, 8u, bk.hb2);  // packed clamp + one multiply-add
-            else
+            } else if constexpr (QM == FT_Q_UMAGIC) {
+                // exact integer decoding of u8 / u16 pairs (ft_lines.cuh); absent cells -> sentinel
+                v = pack_pair_umagic<DT>(src[c], q, 8u, bk.hb2);
+                if constexpr (EDGE) {
+                    const uint32_t keep = (okx ? 0x0000FFFFu : 0u) | (oky ? 0xFFFF0000u : 0u);
+                    v = (v & keep) | (S & ~keep);
+                }
+            } else
                 v = pack_pair<DT, QM, 1>(src[c], !EDGE || okx, !EDGE || oky, tt, q, g.M, sent8) + bk.hb2;
             if (EDGE && !((rowok >> c) & 1u)) v = S;
             V[c] = exists ? v : S;
@@ -309,7 +316,7 @@ __global__ void __launch_bounds__(HM3_NTH, 1) hist3d_march(const typename Elem<D
     uint32_t* ta = h + NROW3 * M2;
     uint32_t* tb = ta + NXT * RP;
     float* tt = reinterpret_cast<float*>(tb + NXT * RP);
-    init_shared3<RP>(h, ta, tb, tt, rt, q, M2, QM != FT_Q_IDENTITY && QM != FT_Q_POW2);
+    init_shared3<RP>(h, ta, tb, tt, rt, q, M2, QM != FT_Q_IDENTITY && QM != FT_Q_POW2 && QM != FT_Q_UMAGIC);
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     Book3 bk;
@@ -482,6 +489,7 @@ static int launch3(const ft_window* win, int64_t H, int64_t W, int64_t D, int64_
     g.H = H; g.W = W; g.D = D; g.v0 = v0; g.v1 = v1; g.first = win->first; g.M = M;
     QuantDev q{qa ? qa->mode : FT_Q_IDENTITY, qa ? qa->negate : 0, qa ? qa->scale : 0.f, qa ? qa->bias : 0.f,
                qa ? qa->thresholds : nullptr};
+    if (QM == FT_Q_UMAGIC && !umagic_fill(qa, M, DT == FT_U8 ? 256 : 65536, q)) return FT_ERR_INTERNAL;
     auto* out = reinterpret_cast<unsigned long long*>(hist);
     const int nsm = sm_count();
     if (march3_ok(M)) {
@@ -506,7 +514,7 @@ static int launch3(const ft_window* win, int64_t H, int64_t W, int64_t D, int64_
     }
     const int64_t n = (v1 - v0) * (W + 1) * (D + 1);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), (int64_t)nsm * 8));
-    constexpr int QW = QM == FT_Q_POW2 ? FT_Q_TABLE : QM;  // the table ships with FT_Q_POW2 too
+    constexpr int QW = QM == FT_Q_POW2 || QM == FT_Q_UMAGIC ? FT_Q_TABLE : QM;  // the table ships with these too
     hist3d_wide<DT, QW><<<grid, 256, 0, st>>>(buf, g, q, rt, out);
     FT_CUDA_TRY(cudaGetLastError());
     return FT_OK;
@@ -558,16 +566,20 @@ extern "C" int ft_hist3d(const ft_window* win, int64_t H, int64_t W, int64_t D, 
     const int qm = effective_qmode(q, true);
     if (qm != FT_Q_IDENTITY && (!q->thresholds || win->dtype == FT_I32)) return FT_ERR_ARG;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    QuantDev probe{};
     switch (win->dtype) {
     case FT_I32:
         if (qm != FT_Q_IDENTITY) return FT_ERR_ARG;
         return launch3<FT_I32, FT_Q_IDENTITY>(win, H, W, D, v0, v1, q, M, hist, st);
     case FT_U8:
         if (qm == FT_Q_IDENTITY) return launch3<FT_U8, FT_Q_IDENTITY>(win, H, W, D, v0, v1, q, M, hist, st);
+        if (march3_ok(M) && umagic_fill(q, M, 256, probe)) return launch3<FT_U8, FT_Q_UMAGIC>(win, H, W, D, v0, v1, q, M, hist, st);
         if (qm == FT_Q_TABLE || qm == FT_Q_POW2) return launch3<FT_U8, FT_Q_TABLE>(win, H, W, D, v0, v1, q, M, hist, st);
         return launch3<FT_U8, FT_Q_TABLE_ROBUST>(win, H, W, D, v0, v1, q, M, hist, st);
     case FT_U16:
         if (qm == FT_Q_IDENTITY) return launch3<FT_U16, FT_Q_IDENTITY>(win, H, W, D, v0, v1, q, M, hist, st);
+        // integer ranges (the data's min / max): exact integer decoding in the march kernel, no table
+        if (march3_ok(M) && umagic_fill(q, M, 65536, probe)) return launch3<FT_U16, FT_Q_UMAGIC>(win, H, W, D, v0, v1, q, M, hist, st);
         if (qm == FT_Q_POW2) return launch3<FT_U16, FT_Q_POW2>(win, H, W, D, v0, v1, q, M, hist, st);
         if (qm == FT_Q_TABLE) return launch3<FT_U16, FT_Q_TABLE>(win, H, W, D, v0, v1, q, M, hist, st);
         return launch3<FT_U16, FT_Q_TABLE_ROBUST>(win, H, W, D, v0, v1, q, M, hist, st);
