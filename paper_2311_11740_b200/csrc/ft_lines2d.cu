@@ -86,6 +86,8 @@ __device__ __forceinline__ void lines2d_item(const typename Elem<DT>::T* __restr
         uint32_t v;
         if constexpr (QM == FT_Q_POW2)
             v = pack_pow2_sat<DT>(src, q.inv, Mf, g.four, sbw);
+        else if constexpr (QM == FT_Q_UMAGIC)
+            v = pack_pair_umagic<DT>(src, q, g.four, sbw);  // u8 / u16 integer ranges: exact integer decoding
         else if constexpr (QM == FT_Q_IDENTITY && (DT == FT_U8 || DT == FT_U16))
             v = pack_pair_ident<DT>(src, sent_lv2, g.four, sbw);
         else
@@ -203,7 +205,7 @@ __global__ void __launch_bounds__(L2L_NTH, MINB) lines2d_kernel(const typename E
     uint32_t* hw = reinterpret_cast<uint32_t*>(h);
     for (int i = threadIdx.x; i < lay.end / 4; i += blockDim.x) hw[i] = 0;
     __syncthreads();
-    if (QM != FT_Q_IDENTITY && QM != FT_Q_POW2)
+    if (QM != FT_Q_IDENTITY && QM != FT_Q_POW2 && QM != FT_Q_UMAGIC)
         for (int i = threadIdx.x; i < M2; i += blockDim.x) tt[i] = q.tt[i];
     __syncthreads();
 
@@ -285,6 +287,7 @@ static int launch_lines2d(const ft_window* win, int64_t H, int64_t W, int64_t v0
                      reinterpret_cast<uintptr_t>(win->data) % (2 * sizeof(T)) == 0;
     QuantDev qd = qdev(qa);
     if (QM == FT_Q_POW2) qd.inv = M > 0 ? qd.scale / (float)M : 0.f;
+    if (QM == FT_Q_UMAGIC && !umagic_fill(qa, M, DT == FT_U8 ? 256 : 65536, qd)) return FT_ERR_INTERNAL;
     const size_t smem = (size_t)lines_layout(g.hs, L2L_SIG, M).end;
     using K = void (*)(const T*, LGeo, QuantDev, unsigned long long*);
     const bool single = g.n_items == 1;
@@ -326,16 +329,19 @@ extern "C" int ft_lines2d(const ft_window* win, int64_t H, int64_t W, int64_t v0
     const int qm = effective_qmode(q, true);
     if (qm != FT_Q_IDENTITY && !q->thresholds) return FT_ERR_ARG;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    QuantDev probe{};
     switch (win->dtype) {
     case FT_I32:
         if (qm != FT_Q_IDENTITY) return FT_ERR_ARG;
         return launch_lines2d<FT_I32, FT_Q_IDENTITY>(win, H, W, v0, v1, q, M, hist, st);
     case FT_U8:
         if (qm == FT_Q_IDENTITY) return launch_lines2d<FT_U8, FT_Q_IDENTITY>(win, H, W, v0, v1, q, M, hist, st);
+        if (umagic_fill(q, M, 256, probe)) return launch_lines2d<FT_U8, FT_Q_UMAGIC>(win, H, W, v0, v1, q, M, hist, st);
         if (qm == FT_Q_TABLE || qm == FT_Q_POW2) return launch_lines2d<FT_U8, FT_Q_TABLE>(win, H, W, v0, v1, q, M, hist, st);
         return launch_lines2d<FT_U8, FT_Q_TABLE_ROBUST>(win, H, W, v0, v1, q, M, hist, st);
     case FT_U16:
         if (qm == FT_Q_IDENTITY) return launch_lines2d<FT_U16, FT_Q_IDENTITY>(win, H, W, v0, v1, q, M, hist, st);
+        if (umagic_fill(q, M, 65536, probe)) return launch_lines2d<FT_U16, FT_Q_UMAGIC>(win, H, W, v0, v1, q, M, hist, st);
         if (qm == FT_Q_POW2) return launch_lines2d<FT_U16, FT_Q_POW2>(win, H, W, v0, v1, q, M, hist, st);
         if (qm == FT_Q_TABLE) return launch_lines2d<FT_U16, FT_Q_TABLE>(win, H, W, v0, v1, q, M, hist, st);
         return launch_lines2d<FT_U16, FT_Q_TABLE_ROBUST>(win, H, W, v0, v1, q, M, hist, st);
